@@ -1,0 +1,375 @@
+"""Benchmark: frames/s of the textured-2DGS render path (BASELINE configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "cfg2"): make_shell_scene(100000, T=8,
+seed=3) with lobe_environment(default_rng(0), 64, 6), 800x800 views from the
+bench_cameras orbit (256 views, each rank takes views r, r+N, ...). One step =
+one frame: K1-K4 binning (preprocess, fp64 depth-rank sort, tile
+duplication + sort, ranges), K5 per-tile textured compositor (atlas fetched
+by the texture units), K6 deferred split-sum shading. Scene, atlas and
+environment are resident in HBM; L2 is flushed (256 MB write) between timed
+steps. Timed with CUDA events on the launch stream, max over ranks.
+
+--impl reference times the reference's CPU implementation of the same path:
+the C oracle port of texsplat's render_forward + shade_gbuffer (oracle/,
+the reference itself is numpy and does not travel), on all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "frames/sec at 800×800 (100k textured 2DGS) 1–8 B200; % TEX/HBM peak"
+WORKLOAD = ("cfg2 (BASELINE configs[1]): 100k textured 2D Gaussians, 8x8 texel atlas, 800x800, "
+            "forward + deferred envmap shading")
+CPU_BASELINE_NOTE = ("C oracle port of texsplat render_forward+shade_gbuffer (fp32, OpenMP over "
+                     "tiles); the numpy reference itself measured 0.0193 fps single-process on "
+                     "the survey host (SURVEY.md §6)")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--splats", type=int, default=100_000)
+    ap.add_argument("--texture-res", type=int, default=8)
+    ap.add_argument("--width", type=int, default=800)
+    ap.add_argument("--height", type=int, default=800)
+    ap.add_argument("--sampler", default="hw", choices=["hw", "verify", "flat"])
+    ap.add_argument("--texel-format", default="rgba32f", choices=["rgba32f", "rgba16f"])
+    ap.add_argument("--tile", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-frames", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_baseline_run(args, frames: int):
+    """Oracle port render+shade on host cores; returns (fps, cores, sample)."""
+    import numpy as np
+    from oracle import oracle
+    from paper_2506_13348_b200 import synth
+    from paper_2506_13348_b200.environment import BrdfLut
+
+    scene = synth.make_shell_scene(args.splats, args.texture_res, seed=3, with_environment=True)
+    cams = synth.bench_cameras(256, args.width, args.height)
+    lut = BrdfLut.build()
+    atlas = oracle.pack(scene.texels)
+    cores = oracle.cpu_threads()
+    mode = "flat" if args.sampler == "flat" else "verify"
+    # one untimed frame (page-in, thread-pool start)
+    r = oracle.render(scene, cams[0], mode=mode, threads=cores, atlas=atlas)
+    times = []
+    for i in range(frames):
+        cam = cams[i % len(cams)]
+        t0 = time.perf_counter()
+        r = oracle.render(scene, cam, mode=mode, threads=cores, atlas=atlas)
+        oracle.shade(r["gbuf"], cam, scene.environment, lut.table, scene.background,
+                     threads=cores)
+        times.append(time.perf_counter() - t0)
+    fps = len(times) / sum(times)
+    sample = (f"{len(times)} full {args.width}x{args.height} frames of the same workload "
+              f"(render_forward+shade_gbuffer), views 0..{len(times) - 1}")
+    return fps, cores, sample, float(np.median(times))
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    frames = max(1, args.steps)
+    for _ in range(min(args.warmup, 1)):
+        pass
+    fps, cores, sample, _ = cpu_baseline_run(args, min(frames, 5))
+    line = {
+        "metric": METRIC, "value": round(fps, 6), "unit": "frames/s", "n_gpus": 0,
+        "steps": min(frames, 5), "warmup": 1, "ms_per_step": round(1e3 / fps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "splats": args.splats, "texture_res": args.texture_res,
+                   "width": args.width, "height": args.height},
+        "cpu_baseline": {"value": round(fps, 6), "unit": "frames/s", "cores": cores,
+                         "kind": "port", "sample": sample, "note": CPU_BASELINE_NOTE},
+        "e2e": {"value": round(fps, 6), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_13348_b200 import Renderer, pack_atlases, synth
+    from paper_2506_13348_b200 import _lib
+    from paper_2506_13348_b200.environment import BrdfLut
+    from paper_2506_13348_b200.rasterize import render_prepared
+    from paper_2506_13348_b200.shading import shade_planar
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    scene = synth.make_shell_scene(args.splats, args.texture_res, seed=3, with_environment=True)
+    cams = synth.bench_cameras(256, args.width, args.height)
+    lut = BrdfLut.build()
+    texture_mode = "flat" if args.sampler == "flat" else "atlas"
+    atlas = pack_atlases(scene) if texture_mode == "atlas" else None
+    r = Renderer(scene, atlas, scene.environment, lut, texture_mode=texture_mode,
+                 sampler=None if args.sampler == "flat" else args.sampler,
+                 texel_format=args.texel_format, tile=args.tile)
+    my_views = [cams[i] for i in range(rank, len(cams), world)]
+
+    # size the workspace from the whole orbit once (no per-frame host sync)
+    need = 0
+    for cam in my_views[:: max(1, len(my_views) // 16)]:
+        r.render(cam, check=True)
+        need = max(need, r.entries_needed())
+    r.reserve(my_views[0], int(need * 1.15) + 4096)
+
+    W, H = args.width, args.height
+    gb, px, col, _, _ = r._buffers(W, H)
+    prep = r.prep
+    L = _lib.lib()
+    stream = torch.cuda.current_stream()
+    sh = _lib.stream_handle(stream)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    ws = prep.workspace
+    mode = {"hw": _lib.MODE_HW, "verify": _lib.MODE_VERIFY, "flat": _lib.MODE_FLAT}[prep.sampler]
+    sc, at = prep.scene.struct(), prep.atlas.struct()
+    import ctypes as C
+
+    def step(cam, evs=None):
+        cs = _lib.camera_struct(cam)
+        pst = px.struct()
+        if evs:
+            evs[0].record(stream)
+        _lib.check(L.tsb_render_binning(C.byref(sc), C.byref(cs), C.byref(at), mode, args.tile,
+                                        _lib.ptr(ws.buf), ws.nbytes, ws.capacity,
+                                        _lib.ptr(ws.needed), sh), "binning")
+        if evs:
+            evs[1].record(stream)
+        _lib.check(L.tsb_render_composite(C.byref(sc), C.byref(cs), C.byref(at), mode, args.tile,
+                                          _lib.ptr(ws.buf), ws.nbytes, ws.capacity,
+                                          _lib.ptr(gb), C.byref(pst), sh), "composite")
+        if evs:
+            evs[2].record(stream)
+        shade_planar(gb, cam, r.env, r.background, color=col, want_split=False, stream=stream)
+        if evs:
+            evs[3].record(stream)
+
+    for i in range(args.warmup):
+        step(my_views[i % len(my_views)])
+    torch.cuda.synchronize()
+
+    K = args.steps
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    frag_total = torch.zeros((), dtype=torch.int64, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(K):
+        flush.zero_()  # L2 flush (outside the timed events)
+        step(my_views[i % len(my_views)], events[i])
+        frag_total += px.n_contrib.sum(dtype=torch.int64)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    frame_ms = [e[0].elapsed_time(e[3]) for e in events]
+    bin_ms = [e[0].elapsed_time(e[1]) for e in events]
+    rast_ms = [e[1].elapsed_time(e[2]) for e in events]
+    shade_ms = [e[2].elapsed_time(e[3]) for e in events]
+    total_ms = sum(frame_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    overflow = r.entries_needed() > ws.capacity
+    fragments = int(frag_total.item()) / K
+
+    # ---- e2e: public API, host result every step ---------------------------
+    host = torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True)
+    cam_bytes = C.sizeof(_lib.Camera_t)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.e2e_steps):
+        c, _ = r.render(my_views[i % len(my_views)], check=False)
+        host.copy_(c, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_fps = world * args.e2e_steps / float(te.item())
+
+    # ---- TEX peak probe (same texture, L1-resident window) ------------------
+    tex_peak = None
+    if prep.atlas.tex is not None:
+        blocks, threads, iters = 148 * 8, 256, 512
+        sink = torch.empty(blocks * threads, dtype=torch.float32, device=dev)
+        for _ in range(2):
+            _lib.check(L.tsb_tex_probe(prep.atlas.tex, 32, iters, _lib.ptr(sink), blocks, threads,
+                                       sh), "tex probe")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        reps = 5
+        for _ in range(reps):
+            L.tsb_tex_probe(prep.atlas.tex, 32, iters, _lib.ptr(sink), blocks, threads, sh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tex_peak = reps * blocks * threads * iters / (e0.elapsed_time(e1) * 1e-3) / 1e9  # Gfetch/s
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    import json as _json
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = _json.loads(pk.read_text())
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    rast_avg_s = statistics.mean(rast_ms) * 1e-3
+    T = args.texture_res
+    P = args.splats
+    texel_b = 16 if args.texel_format == "rgba32f" else 8
+    # compulsory HBM bytes of one K5 launch: G-buffer
+    # + pixel state out, entry list + per-splat records in, and the atlas
+    # charts of every splat (both families) read once.
+    entries = r.entries_needed()
+    alg_bytes = 68 * W * H + 4 * entries + 128 * P + 2 * P * T * T * texel_b
+    hbm_achieved = alg_bytes / rast_avg_s / 1e9
+    fetch_rate = 2 * fragments / rast_avg_s / 1e9 if args.sampler != "flat" else 0.0
+
+    value = world * K / (max_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(max_ms / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "splats": P, "texture_res": T, "width": W,
+                   "height": H, "sampler": args.sampler, "texel_format": args.texel_format,
+                   "tile": args.tile, "views": "bench_cameras(256) orbit, rank r takes r::N",
+                   "l2": "flushed between timed steps (256 MB write, outside the events)",
+                   "parallelism": f"views partitioned over {world} GPU(s), scene replicated"},
+        "breakdown_ms": {"binning": round(statistics.mean(bin_ms), 4),
+                         "raster": round(statistics.mean(rast_ms), 4),
+                         "shade": round(statistics.mean(shade_ms), 4),
+                         "frame_median": round(statistics.median(frame_ms), 4)},
+        "fragments_per_frame": fragments, "entries_per_frame": entries,
+        "capacity_overflow": bool(overflow),
+        "roofline": {"bound": "hbm", "kernel": "k_raster_fwd", "achieved": round(hbm_achieved, 2),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(hbm_achieved / hbm_peak, 4),
+                     "traffic": None, "peak_source": hbm_src,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "roofline_tex": {"bound": "tex", "kernel": "k_raster_fwd",
+                         "achieved": round(fetch_rate, 3), "unit": "Gfetch/s",
+                         "peak": round(tex_peak, 3) if tex_peak else None,
+                         "frac": round(fetch_rate / tex_peak, 4) if tex_peak else None,
+                         "peak_source": "measured live: tsb_tex_probe bilinear RGBA fetches, "
+                                        "L1-resident 32x32 window of the same texture",
+                         "fetches_per_launch": 2 * fragments},
+        "clocks": clk,
+        "e2e": {"value": round(e2e_fps, 3), "unit": "frames/s",
+                "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": H * W * 3 * 4,
+                "note": "Renderer.render(camera) -> colour copied to pinned host memory and "
+                        "synchronised every step; camera passed by value in the launch; scene, "
+                        "atlas, environment resident (uploaded once)"},
+        "gpu_launches": 6 * K,
+        "gpu_launches_note": "ours per frame: k_preprocess, k_rank_counts, k_duplicate, "
+                             "k_ranges, k_raster_fwd, k_shade (+ CUB radix sort/scan kernels)",
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        fps, cores, sample, _ = cpu_baseline_run(args, args.cpu_frames)
+        line["cpu_baseline"] = {"value": round(fps, 6), "unit": "frames/s", "cores": cores,
+                                "kind": "port", "sample": sample, "note": CPU_BASELINE_NOTE}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

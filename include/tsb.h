@@ -1,0 +1,177 @@
+/*
+ * tsb.h — C ABI of libtsb.so, the B200 (sm_100a) textured-2DGS render path.
+ *
+ * The library allocates no device memory for frame data: the caller (PyTorch
+ * in the Python host layer, or any C/C++ host) owns every buffer and passes
+ * raw device pointers, a CUDA stream and a workspace sized by
+ * tsb_frame_workspace_size(). The only library-owned device objects are the
+ * cudaArray/texture objects behind a tsb_atlas_tex_t (tsb_atlas_tex_create).
+ * Nothing synchronises the host; errors from launches are reported through
+ * the return code (cudaGetLastError after each launch) and tsb_last_error().
+ *
+ * The reference (/root/reference/pkg/src/texsplat, pure numpy) has no FFI;
+ * each entry point below replaces one Python callable of its hot path, cited
+ * at the declaration. The Python binding is paper_2506_13348_b200/_lib.py
+ * (ctypes); INTEGRATION.md shows the binding a texsplat maintainer would add.
+ */
+#ifndef TSB_H
+#define TSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes. The Python shim maps them to the reference's exceptions. */
+#define TSB_OK 0
+#define TSB_ERR_VALUE (-1)    /* ValueError   (bad mode, shapes, resolution) */
+#define TSB_ERR_LOOKUP (-2)   /* LookupError  (bad atlas entry / page)       */
+#define TSB_ERR_CUDA (-3)     /* RuntimeError (launch / CUDA API failure)     */
+#define TSB_ERR_CAPACITY (-4) /* workspace smaller than tsb_frame_workspace_size */
+
+/* Texture modes (rasterize.py:172-236 "perprim"/"atlas"/"flat").
+ * HW: atlas fetched by the texture units (tex2DLayered, bilinear).
+ * VERIFY: fp32 software bilinear from linear atlas pages (bit-exact with oracle).
+ * FLAT: per-splat mean texels (rasterize.py:203-209). */
+#define TSB_MODE_HW 0
+#define TSB_MODE_VERIFY 1
+#define TSB_MODE_FLAT 2
+
+/* Atlas texel formats for the HW mode. */
+#define TSB_TEXEL_RGBA32F 0
+#define TSB_TEXEL_RGBA16F 1
+
+/* splats.py:45-78 Camera. world_to_view is row-major 4x4. */
+typedef struct tsb_camera {
+  double world_to_view[16];
+  double fx, fy, cx, cy, near_z, far_z;
+  int32_t width, height;
+} tsb_camera;
+
+/* scene.py:52-77 Scene parameter arrays (float64, device pointers). */
+typedef struct tsb_scene {
+  int32_t num_splats;
+  int32_t sh_degree;           /* 0..3; sh has (deg+1)^2 x 3 values per splat */
+  const double* positions;     /* P x 3 */
+  const double* tangent_u;     /* P x 3 */
+  const double* tangent_v;     /* P x 3 */
+  const double* scales;        /* P x 2 */
+  const double* opacities;     /* P     */
+  const double* sh;            /* P x K x 3 */
+} tsb_scene;
+
+typedef struct tsb_atlas_tex* tsb_atlas_tex_t;
+
+/* atlas.py:35-105 AtlasSet: family A = [albedo.rgb, roughness],
+ * family B = [normal.a, normal.b, metallic, 0], pages of page_h x page_w
+ * RGBA float32 texels, indirection entries (chart_x, chart_y, page). */
+typedef struct tsb_atlas {
+  int32_t resolution;          /* T: texels per chart side */
+  int32_t page_w, page_h, pages;
+  const int32_t* entries;      /* P x 3 device */
+  const float* family_a;       /* pages x page_h x page_w x 4 device (VERIFY) */
+  const float* family_b;       /* same layout (VERIFY) */
+  const float* flat_attrs;     /* P x 5: mean albedo rgb, metallic, roughness (FLAT) */
+  tsb_atlas_tex_t tex;         /* from tsb_atlas_tex_create (HW), may be NULL otherwise */
+} tsb_atlas;
+
+/* environment.py:209-224 EnvironmentLight + BrdfLut (device, float32). */
+#define TSB_ENV_MAX_LEVELS 16
+typedef struct tsb_environment {
+  int32_t levels;
+  const float* spec_mips[TSB_ENV_MAX_LEVELS];  /* level l: mip_h[l] x mip_w[l] x 3 */
+  int32_t mip_h[TSB_ENV_MAX_LEVELS];
+  int32_t mip_w[TSB_ENV_MAX_LEVELS];
+  const float* diffuse;                        /* diff_h x diff_w x 3 */
+  int32_t diff_h, diff_w;
+  const float* lut;                            /* lut_res x lut_res x 2 */
+  int32_t lut_res;
+} tsb_environment;
+
+/* Per-pixel forward state (all H x W, device). Kept for the backward pass
+ * (replaces the reference's Python tape, rasterize.py:383-384). */
+typedef struct tsb_pixel_state {
+  int32_t* n_contrib;   /* composited fragments per pixel */
+  int32_t* last_entry;  /* sorted-entry index of the last contributor, -1 if none */
+  float* final_T;       /* transmittance after the last contributor */
+  float* T_last;        /* transmittance in front of the last contributor */
+} tsb_pixel_state;
+
+/* Bytes of frame workspace for P splats at W x H with `max_entries`
+ * splat x tile entries. The workspace persists from tsb_render_forward to
+ * tsb_render_backward of the same frame. */
+int tsb_frame_workspace_size(int32_t num_splats, int32_t width, int32_t height,
+                             int32_t tile, int64_t max_entries, uint64_t* bytes);
+
+/* Whole forward pass K1-K5 (replaces rasterize.prepare rasterize.py:172-243,
+ * _tile_lists :246-258 and render_forward :395-438): preprocess, fp64
+ * depth-rank sort, tile duplication, stable tile sort, tile ranges and the
+ * per-tile compositor into a planar 13 x H x W float32 G-buffer
+ * (rasterize.py:52-59 channel map, coverage-premultiplied).
+ * entries_needed (device int64) receives the splat x tile entry count; if it
+ * exceeds max_entries the frame is incomplete and must be re-rendered with a
+ * larger workspace. tile is 8, 16 or 32. */
+int tsb_render_forward(const tsb_scene* scene, const tsb_camera* camera,
+                       const tsb_atlas* atlas, int32_t mode, int32_t tile,
+                       void* workspace, uint64_t workspace_bytes,
+                       int64_t max_entries, float* gbuf,
+                       const tsb_pixel_state* pixels, int64_t* entries_needed,
+                       void* stream);
+
+/* The two halves of tsb_render_forward, for callers that time or overlap
+ * them separately: binning = K1-K4 (prepare + _tile_lists, rasterize.py:
+ * 172-258), composite = K5 (the _render_tile loop, rasterize.py:320-385)
+ * reading the lists binning left in the workspace. */
+int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera,
+                       const tsb_atlas* atlas, int32_t mode, int32_t tile,
+                       void* workspace, uint64_t workspace_bytes,
+                       int64_t max_entries, int64_t* entries_needed, void* stream);
+int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera,
+                         const tsb_atlas* atlas, int32_t mode, int32_t tile,
+                         void* workspace, uint64_t workspace_bytes,
+                         int64_t max_entries, float* gbuf,
+                         const tsb_pixel_state* pixels, void* stream);
+
+/* Copy the frame's structural results out of the workspace (debug/parity):
+ * sorted_ids (P, kept splats in draw order then culled ids), keys
+ * (max_entries: (tile << 32) | depth_rank of every sorted entry, padding
+ * entries = -1) and ranges (num_tiles x 2 [start, end)). Any may be NULL. */
+int tsb_frame_export(int32_t num_splats, int32_t width, int32_t height, int32_t tile,
+                     int64_t max_entries, const void* workspace,
+                     int32_t* sorted_ids, int64_t* keys, int32_t* ranges,
+                     int32_t* rects, void* stream);
+
+/* Deferred split-sum shading (replaces shading.shade_gbuffer shading.py:126-183
+ * with mesh=None). gbuf planar 13 x H x W; color/diffuse/specular H x W x 3
+ * (diffuse/specular may be NULL). background: 3 floats (host). */
+int tsb_shade_forward(const float* gbuf, const tsb_camera* camera,
+                      const tsb_environment* env, const float* background,
+                      float* color, float* diffuse, float* specular, void* stream);
+
+/* K0: upload both atlas families (device linear pages, float32 RGBA) into
+ * layered cudaArrays bound to bilinear texture objects (replaces the
+ * 8-channel page concatenation of rasterize.py:225-236). */
+int tsb_atlas_tex_create(const float* family_a, const float* family_b, int32_t page_w,
+                         int32_t page_h, int32_t pages, int32_t texel_format,
+                         tsb_atlas_tex_t* out, void* stream);
+int tsb_atlas_tex_destroy(tsb_atlas_tex_t tex);
+
+/* TEX-unit throughput probe used by bench.py for the TEX roofline: `fetches`
+ * bilinear RGBA fetches spread over an L1-resident window of the atlas.
+ * Writes a checksum per thread into sink (grid*block floats). */
+int tsb_tex_probe(tsb_atlas_tex_t tex, int32_t window, int32_t iters, float* sink,
+                  int32_t blocks, int32_t threads, void* stream);
+
+/* Last error message of the calling thread. */
+const char* tsb_last_error(void);
+
+/* Library version string. */
+const char* tsb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSB_H */

@@ -1,0 +1,238 @@
+"""Device-resident inputs and frame workspace for libtsb.
+
+PyTorch owns every device buffer (plumbing only); libtsb receives raw
+pointers. Layouts:
+  DeviceScene        float64 SoA: positions/t_u/t_v (P,3), scales (P,2),
+                     opacities (P,), sh (P,K,3)       — scene.py:52-77
+  DeviceAtlas        family A/B pages (pages, page_h, page_w, 4) float32,
+                     indirection (P,3) int32, flat attrs (P,5) float32, and
+                     the layered texture objects (RGBA32F or RGBA16F)
+  DeviceEnvironment  spec mips (h_l, w_l, 3), diffuse (h, w, 3), LUT (r, r, 2), float32
+  FrameWorkspace     one byte buffer carved by tsb_frame_workspace_size()
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .atlas import AtlasSet, pack_texels
+from .scene import flat_attrs, scene_texels
+
+
+def _dev(device):
+    if device is None:
+        if not torch.cuda.is_available():
+            raise _lib.TsbError("libtsb needs a CUDA device (no CPU fallback)")
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+class DeviceScene:
+    """Splat parameters resident in HBM (float64, the reference's dtype)."""
+
+    def __init__(self, scene, device=None):
+        dev = _dev(device)
+        self.device = dev
+        self.num_splats = int(scene.positions.shape[0])
+        self.sh_degree = int(scene.sh_degree)
+        if not 0 <= self.sh_degree <= 3:
+            raise ValueError("SH degree must be in [0, 3]")
+
+        def up(a, shape):
+            a = np.ascontiguousarray(a, dtype=np.float64).reshape(shape)
+            return torch.from_numpy(a).to(dev, non_blocking=False)
+
+        P = self.num_splats
+        K = (self.sh_degree + 1) ** 2
+        self.positions = up(scene.positions, (P, 3))
+        self.tangent_u = up(scene.tangent_u, (P, 3))
+        self.tangent_v = up(scene.tangent_v, (P, 3))
+        self.scales = up(scene.scales, (P, 2))
+        self.opacities = up(scene.opacities, (P,))
+        self.sh = up(scene.sh, (P, K, 3))
+        self.texture_resolution = int(scene.texture_config.resolution)
+
+    @staticmethod
+    def from_tensors(positions, tangent_u, tangent_v, scales, opacities, sh, sh_degree,
+                     texture_resolution):
+        self = DeviceScene.__new__(DeviceScene)
+        self.device = positions.device
+        self.num_splats = int(positions.shape[0])
+        self.sh_degree = int(sh_degree)
+        self.positions, self.tangent_u, self.tangent_v = positions, tangent_u, tangent_v
+        self.scales, self.opacities, self.sh = scales, opacities, sh
+        self.texture_resolution = int(texture_resolution)
+        return self
+
+    def struct(self) -> _lib.Scene_t:
+        s = _lib.Scene_t()
+        s.num_splats = self.num_splats
+        s.sh_degree = self.sh_degree
+        s.positions = _lib.ptr(self.positions)
+        s.tangent_u = _lib.ptr(self.tangent_u)
+        s.tangent_v = _lib.ptr(self.tangent_v)
+        s.scales = _lib.ptr(self.scales)
+        s.opacities = _lib.ptr(self.opacities)
+        s.sh = _lib.ptr(self.sh)
+        return s
+
+
+_FORMATS = {"rgba32f": _lib.TEXEL_RGBA32F, "rgba16f": _lib.TEXEL_RGBA16F}
+
+
+class DeviceAtlas:
+    """Atlas pages in HBM: linear copies (verify mode) and/or layered
+    texture objects (HW mode), plus flat-mode per-splat means."""
+
+    def __init__(self, atlas_set: AtlasSet = None, *, texels=None, linear=True, hw=True,
+                 texel_format="rgba32f", flat=False, device=None):
+        dev = _dev(device)
+        self.device = dev
+        if atlas_set is None:
+            if texels is None:
+                raise ValueError("DeviceAtlas needs an atlas_set or texels")
+            atlas_set = pack_texels(texels)
+        ind = atlas_set.indirection
+        ind.validate()
+        self.resolution = int(atlas_set.resolution)
+        pa = np.stack([p.texels for p in atlas_set.family_a]).astype(np.float32, copy=False)
+        pb = np.stack([p.texels for p in atlas_set.family_b]).astype(np.float32, copy=False)
+        self.pages, self.page_h, self.page_w = int(pa.shape[0]), int(pa.shape[1]), int(pa.shape[2])
+        if self.pages * self.page_h * self.page_w >= 2 ** 31:
+            raise ValueError("atlas larger than 2^31 texels per family")
+        self.entries = torch.from_numpy(np.ascontiguousarray(ind.entries, np.int32)).to(dev)
+        self.num_entries = int(ind.entries.shape[0])
+        fa = torch.from_numpy(np.ascontiguousarray(pa)).to(dev)
+        fb = torch.from_numpy(np.ascontiguousarray(pb)).to(dev)
+        self.family_a = fa if linear else None
+        self.family_b = fb if linear else None
+        self.texel_format = texel_format
+        self.tex = None
+        if hw:
+            if texel_format not in _FORMATS:
+                raise ValueError(f"unknown texel format {texel_format!r}")
+            h = C.c_void_p()
+            _lib.check(_lib.lib().tsb_atlas_tex_create(
+                _lib.ptr(fa), _lib.ptr(fb), self.page_w, self.page_h, self.pages,
+                _FORMATS[texel_format], C.byref(h), _lib.stream_handle()),
+                "tsb_atlas_tex_create")
+            torch.cuda.current_stream().synchronize()
+            self.tex = h
+        self.flat = None
+        if flat is not False:
+            fl = flat if isinstance(flat, np.ndarray) else None
+            if fl is None:
+                raise ValueError("flat=True needs the (P, 5) flat attribute array")
+            self.flat = torch.from_numpy(np.ascontiguousarray(fl, np.float32)).to(dev)
+
+    @staticmethod
+    def flat_only(texels, device=None) -> "DeviceAtlas":
+        self = DeviceAtlas.__new__(DeviceAtlas)
+        dev = _dev(device)
+        self.device = dev
+        self.resolution = int(texels.shape[1])
+        self.pages = self.page_h = self.page_w = 0
+        self.entries = None
+        self.num_entries = int(texels.shape[0])
+        self.family_a = self.family_b = None
+        self.texel_format = None
+        self.tex = None
+        self.flat = torch.from_numpy(flat_attrs(texels)).to(dev)
+        return self
+
+    def struct(self) -> _lib.Atlas_t:
+        a = _lib.Atlas_t()
+        a.resolution = self.resolution
+        a.page_w, a.page_h, a.pages = self.page_w, self.page_h, self.pages
+        a.entries = _lib.ptr(self.entries)
+        a.family_a = _lib.ptr(self.family_a)
+        a.family_b = _lib.ptr(self.family_b)
+        a.flat_attrs = _lib.ptr(self.flat)
+        a.tex = self.tex.value if self.tex is not None else None
+        return a
+
+    def close(self):
+        if self.tex is not None and self.tex.value:
+            _lib.lib().tsb_atlas_tex_destroy(self.tex)
+            self.tex = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceEnvironment:
+    """Environment mips, irradiance map and split-sum LUT in HBM (float32)."""
+
+    def __init__(self, env, lut, device=None):
+        dev = _dev(device)
+        self.device = dev
+        if env.levels < 1 or env.levels > _lib.ENV_MAX_LEVELS:
+            raise ValueError(f"environment needs 1..{_lib.ENV_MAX_LEVELS} levels")
+        self.mips = [torch.from_numpy(np.ascontiguousarray(m, np.float32)).to(dev)
+                     for m in env.spec_mips]
+        self.diffuse = torch.from_numpy(np.ascontiguousarray(env.diffuse, np.float32)).to(dev)
+        table = np.ascontiguousarray(lut.table, np.float32)
+        self.lut = torch.from_numpy(table).to(dev)
+        self.lut_res = int(table.shape[0])
+
+    @staticmethod
+    def from_tensors(mips, diffuse, lut):
+        self = DeviceEnvironment.__new__(DeviceEnvironment)
+        self.device = diffuse.device
+        self.mips, self.diffuse, self.lut = list(mips), diffuse, lut
+        self.lut_res = int(lut.shape[0])
+        return self
+
+    @property
+    def levels(self) -> int:
+        return len(self.mips)
+
+    def struct(self) -> _lib.Environment_t:
+        e = _lib.Environment_t()
+        e.levels = len(self.mips)
+        for i, m in enumerate(self.mips):
+            e.spec_mips[i] = _lib.ptr(m)
+            e.mip_h[i] = int(m.shape[0])
+            e.mip_w[i] = int(m.shape[1])
+        e.diffuse = _lib.ptr(self.diffuse)
+        e.diff_h, e.diff_w = int(self.diffuse.shape[0]), int(self.diffuse.shape[1])
+        e.lut = _lib.ptr(self.lut)
+        e.lut_res = self.lut_res
+        return e
+
+
+class FrameWorkspace:
+    """Frame workspace (sort buffers, per-splat records, tile lists) sized for
+    `capacity` splat x tile entries; grown when a frame needs more."""
+
+    def __init__(self, device=None):
+        self.device = _dev(device)
+        self.key = None
+        self.capacity = 0
+        self.buf = None
+        self.nbytes = 0
+        self.needed = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def ensure(self, P, W, H, tile, capacity):
+        key = (P, W, H, tile)
+        if self.key == key and self.capacity >= capacity:
+            return
+        cap = max(int(capacity), 1)
+        nb = C.c_uint64()
+        _lib.check(_lib.lib().tsb_frame_workspace_size(P, W, H, tile, cap, C.byref(nb)),
+                   "tsb_frame_workspace_size")
+        self.buf = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
+        self.nbytes = int(nb.value)
+        self.capacity = cap
+        self.key = key
+
+    @staticmethod
+    def initial_capacity(P, W, H, tile):
+        return int(16 * P + 4 * ((W + tile - 1) // tile) * ((H + tile - 1) // tile) + 4096)
