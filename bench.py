@@ -85,6 +85,9 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10.0:
+                time.sleep(0.05)
         except OSError:
             self.proc = None
 
@@ -253,7 +256,6 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
     frame_ms = [e[0].elapsed_time(e[3]) for e in events]
     bin_ms = [e[0].elapsed_time(e[1]) for e in events]
     rast_ms = [e[1].elapsed_time(e[2]) for e in events]
@@ -276,6 +278,7 @@ def main():
         host.copy_(c, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     e2e_s = time.perf_counter() - t0
+    clk = clocks.stop()
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)

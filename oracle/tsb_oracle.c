@@ -42,8 +42,7 @@ typedef struct oracle_frame {
   int64_t num_entries;
   tsb_cam_params cam;
   /* per splat (by id) */
-  float* geom_m;       /* P x 9 fp32 M */
-  float* opacity_f;    /* P */
+  float* lin;          /* P x TSB_LIN_WORDS linear intersection forms */
   double* m64;         /* P x 10 (M + opacity) */
   int32_t* rects;      /* P x 4 */
   float* frame;        /* P x 9 */
@@ -69,7 +68,7 @@ static int cmp_z_id(const void* a, const void* b) {
 
 void oracle_frame_free(oracle_frame* f) {
   if (!f) return;
-  free(f->geom_m); free(f->opacity_f); free(f->m64); free(f->rects); free(f->frame);
+  free(f->lin); free(f->m64); free(f->rects); free(f->frame);
   free(f->l_ind); free(f->view_z); free(f->keep); free(f->rank); free(f->sorted_ids);
   free(f->ranges); free(f->entry_ids); free(f->keys);
   free(f);
@@ -88,8 +87,7 @@ oracle_frame* oracle_frame_new(int32_t P, int32_t sh_degree, const double* posit
   f->tiles_y = (f->H + tile - 1) / tile;
   f->num_tiles = f->tiles_x * f->tiles_y;
   size_t Pn = P > 0 ? (size_t)P : 1;
-  f->geom_m = (float*)malloc(Pn * 9 * sizeof(float));
-  f->opacity_f = (float*)malloc(Pn * sizeof(float));
+  f->lin = (float*)malloc(Pn * TSB_LIN_WORDS * sizeof(float));
   f->m64 = (double*)malloc(Pn * 10 * sizeof(double));
   f->rects = (int32_t*)malloc(Pn * 4 * sizeof(int32_t));
   f->frame = (float*)malloc(Pn * 9 * sizeof(float));
@@ -109,13 +107,12 @@ oracle_frame* oracle_frame_new(int32_t P, int32_t sh_degree, const double* posit
     tsb_preprocess_splat(cam, positions + 3 * (size_t)id, tangent_u + 3 * (size_t)id,
                          tangent_v + 3 * (size_t)id, scales + 2 * (size_t)id,
                          sh + (size_t)3 * K * id, sh_degree, &r);
+    tsb_make_lin(r.m, opacities[id], f->lin + TSB_LIN_WORDS * (size_t)id);
     for (int k = 0; k < 9; ++k) {
-      f->geom_m[9 * (size_t)id + k] = (float)r.m[k];
       f->m64[10 * (size_t)id + k] = r.m[k];
       f->frame[9 * (size_t)id + k] = (float)r.frame[k];
     }
     f->m64[10 * (size_t)id + 9] = opacities[id];
-    f->opacity_f[id] = (float)opacities[id];
     for (int k = 0; k < 3; ++k) f->l_ind[3 * (size_t)id + k] = (float)r.l_ind[k];
     f->rects[4 * (size_t)id] = r.x0; f->rects[4 * (size_t)id + 1] = r.x1;
     f->rects[4 * (size_t)id + 2] = r.y0; f->rects[4 * (size_t)id + 3] = r.y1;
@@ -227,8 +224,7 @@ void oracle_frame_raster(const oracle_frame* f, int32_t mode, int32_t T, int32_t
         const int rx0 = rc[0] > tx0 ? rc[0] : tx0, rx1 = rc[1] < tx1 ? rc[1] : tx1;
         const int ry0 = rc[2] > ty0 ? rc[2] : ty0, ry1 = rc[3] < ty1 ? rc[3] : ty1;
         if (rx0 >= rx1 || ry0 >= ry1) continue;
-        const float* m = f->geom_m + 9 * (size_t)id;
-        const float op = f->opacity_f[id];
+        const float* lin = f->lin + TSB_LIN_WORDS * (size_t)id;
         const float* fr = f->frame + 9 * (size_t)id;
         for (int py = ry0; py < ry1; ++py) {
           const double yd = tsb_pixel_y(&f->cam, py);
@@ -239,7 +235,7 @@ void oracle_frame_raster(const oracle_frame* f, int32_t mode, int32_t T, int32_t
             const double xd = tsb_pixel_x(&f->cam, px);
             const float x = (float)xd;
             float u, v, z, a;
-            int r = tsb_intersect_f32(m, op, x, y, near_f, &u, &v, &z, &a);
+            int r = tsb_eval_lin(lin, x, y, near_f, &u, &v, &z, &a);
             if (r == 0) continue;
             if (r == 2) {
               const double* m64 = f->m64 + 10 * (size_t)id;

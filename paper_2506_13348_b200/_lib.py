@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libtsb.so"
+LIB_PATH = Path(os.environ.get("TSB_LIB", str(_HERE / "libtsb.so")))
 
 TSB_OK = 0
 TSB_ERR_VALUE = -1

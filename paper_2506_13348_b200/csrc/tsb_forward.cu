@@ -27,6 +27,11 @@
 
 #include "tsb_internal.cuh"
 
+// Minimum resident CTAs per SM requested for the 16x16 rasterizer.
+#ifndef TSB_RASTER_MINB
+#define TSB_RASTER_MINB 2
+#endif
+
 namespace tsb {
 
 static thread_local std::string g_err;
@@ -67,6 +72,7 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
   L->geom = take(Pn * sizeof(GeomRec));
+  L->rects = take(Pn * 8);
   L->mat = take(Pn * sizeof(MatRec));
   L->m64 = take(Pn * kM64Stride * sizeof(double));
   L->dkeys_in = take(Pn * 8);
@@ -103,6 +109,7 @@ struct PrepParams {
   const int32_t* entries;   // may be null (flat mode)
   int32_t T, page_w, page_h;
   GeomRec* geom;
+  uint2* rects;
   MatRec* mat;
   double* m64;
   uint64_t* dkeys;
@@ -128,9 +135,13 @@ __global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
   const double op = p.op[id];
 
   GeomRec g;
-  for (int k = 0; k < 9; ++k) g.m[k] = (float)r.m[k];
-  g.opacity = (float)op;
-  g.x0 = r.x0; g.x1 = r.x1; g.y0 = r.y0; g.y1 = r.y1;
+  tsb_make_lin(r.m, op, g.lin);
+  p.rects[id] = make_uint2((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
+                           (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
+  int32_t tb[4];
+  tsb_test_box(&p.cam, r.m, g.lin[11], r.x0, r.x1, r.y0, r.y1, tb);
+  g.bx = (uint32_t)tb[0] | ((uint32_t)tb[1] << 16);
+  g.by = (uint32_t)tb[2] | ((uint32_t)tb[3] << 16);
   g.id = id;
   g.pad = 0;
   p.geom[id] = g;
@@ -175,7 +186,7 @@ __global__ void k_duplicate(int32_t P, int32_t tile, int32_t tiles_x, int64_t ca
                             const int32_t* __restrict__ sorted_ids,
                             const int32_t* __restrict__ counts_sorted,
                             const int32_t* __restrict__ offsets,
-                            const GeomRec* __restrict__ geom, uint32_t* __restrict__ ekeys,
+                            const uint2* __restrict__ rects, uint32_t* __restrict__ ekeys,
                             int32_t* __restrict__ evals, int64_t* __restrict__ counters) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= P) return;
@@ -184,10 +195,11 @@ __global__ void k_duplicate(int32_t P, int32_t tile, int32_t tiles_x, int64_t ca
   if (r == P - 1) counters[0] = off + cnt;
   if (cnt == 0 || off + cnt > cap) return;
   const int id = sorted_ids[r];
-  const GeomRec g = geom[id];
+  const uint2 rc = rects[id];
+  const int x0 = rc.x & 0xFFFF, x1 = rc.x >> 16, y0 = rc.y & 0xFFFF, y1 = rc.y >> 16;
   int64_t o = off;
-  for (int ty = g.y0 / tile; ty <= (g.y1 - 1) / tile; ++ty)
-    for (int tx = g.x0 / tile; tx <= (g.x1 - 1) / tile; ++tx) {
+  for (int ty = y0 / tile; ty <= (y1 - 1) / tile; ++ty)
+    for (int tx = x0 / tile; tx <= (x1 - 1) / tile; ++tx) {
       ekeys[o] = (uint32_t)(ty * tiles_x + tx);
       evals[o] = id;
       ++o;
@@ -232,112 +244,316 @@ struct RasterParams {
   float* T_last;
 };
 
+// A fragment's texel data in flight: the two atlas families (HW / verify)
+// or the flat attributes, plus the fragment's u, v, z, alpha.
+struct Frag {
+  float4 A, B;
+  float z, a;
+};
+
+// Issue the texel reads of fragment (u, v) of splat material `m`. In HW mode
+// these are two bilinear tex2DLayered fetches; verify mode reads the four
+// corners of both families and applies tsb_lerp4 (== lerp_corners).
 template <int MODE>
-__device__ __forceinline__ void fetch_attrs(const RasterParams& p, int id, float u, float v,
-                                            float z, float* xa) {
-  const float4* mr = reinterpret_cast<const float4*>(p.mat + id);
-  const float4 q0 = __ldg(mr), q1 = __ldg(mr + 1), q2 = __ldg(mr + 2);
-  const float frame[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+__device__ __forceinline__ void frag_fetch(const RasterParams& p, const MatRec& m, int id,
+                                           float u, float v, Frag& f) {
   if (MODE == TSB_MODE_FLAT) {
-    const float* f = p.flat + 5 * id;
-    xa[0] = __ldg(f); xa[1] = __ldg(f + 1); xa[2] = __ldg(f + 2);
-    xa[3] = __ldg(f + 3); xa[4] = __ldg(f + 4);
-    xa[5] = frame[6]; xa[6] = frame[7]; xa[7] = frame[8];
-  } else {
-    const float4 q3 = __ldg(mr + 3);
-    tsb_texc tc;
-    tsb_texel_coords(u, v, p.T, &tc);
-    float4 A, B;
-    if (MODE == TSB_MODE_HW) {
-      const float sx = q3.x + tc.xs + 0.5f;
-      const float sy = q3.y + tc.yt + 0.5f;
-      const int layer = __float_as_int(q3.z);
-      A = tex2DLayered<float4>(p.tex_a, sx, sy, layer);
-      B = tex2DLayered<float4>(p.tex_b, sx, sy, layer);
-    } else {
-      const int base = __float_as_int(q3.w);
-      const int r0 = base + tc.j0 * p.page_w, r1 = base + tc.j1 * p.page_w;
-      const float4 a00 = __ldg(p.fam_a + r0 + tc.i0), a01 = __ldg(p.fam_a + r0 + tc.i1);
-      const float4 a10 = __ldg(p.fam_a + r1 + tc.i0), a11 = __ldg(p.fam_a + r1 + tc.i1);
-      const float4 b00 = __ldg(p.fam_b + r0 + tc.i0), b01 = __ldg(p.fam_b + r0 + tc.i1);
-      const float4 b10 = __ldg(p.fam_b + r1 + tc.i0), b11 = __ldg(p.fam_b + r1 + tc.i1);
-      A.x = tsb_lerp4(a00.x, a01.x, a10.x, a11.x, tc.fs, tc.ft);
-      A.y = tsb_lerp4(a00.y, a01.y, a10.y, a11.y, tc.fs, tc.ft);
-      A.z = tsb_lerp4(a00.z, a01.z, a10.z, a11.z, tc.fs, tc.ft);
-      A.w = tsb_lerp4(a00.w, a01.w, a10.w, a11.w, tc.fs, tc.ft);
-      B.x = tsb_lerp4(b00.x, b01.x, b10.x, b11.x, tc.fs, tc.ft);
-      B.y = tsb_lerp4(b00.y, b01.y, b10.y, b11.y, tc.fs, tc.ft);
-      B.z = tsb_lerp4(b00.z, b01.z, b10.z, b11.z, tc.fs, tc.ft);
-      B.w = 0.f;
-    }
-    xa[0] = A.x; xa[1] = A.y; xa[2] = A.z;
-    xa[3] = B.z;  // metallic
-    xa[4] = A.w;  // roughness
-    tsb_decode_normal(B.x, B.y, frame, xa + 5);
+    const float* fl = p.flat + 5 * id;
+    f.A = make_float4(__ldg(fl), __ldg(fl + 1), __ldg(fl + 2), __ldg(fl + 4));
+    f.B = make_float4(0.f, 0.f, __ldg(fl + 3), 0.f);
+    return;
   }
-  xa[8] = q2.y; xa[9] = q2.z; xa[10] = q2.w;
-  xa[11] = z;
+  tsb_texc tc;
+  tsb_texel_coords(u, v, p.T, &tc);
+  if (MODE == TSB_MODE_HW) {
+    const float sx = m.tex_x + tc.xs + 0.5f;
+    const float sy = m.tex_y + tc.yt + 0.5f;
+    f.A = tex2DLayered<float4>(p.tex_a, sx, sy, m.page);
+    f.B = tex2DLayered<float4>(p.tex_b, sx, sy, m.page);
+  } else {
+    const int r0 = m.lin_off + tc.j0 * p.page_w, r1 = m.lin_off + tc.j1 * p.page_w;
+    const float4 a00 = __ldg(p.fam_a + r0 + tc.i0), a01 = __ldg(p.fam_a + r0 + tc.i1);
+    const float4 a10 = __ldg(p.fam_a + r1 + tc.i0), a11 = __ldg(p.fam_a + r1 + tc.i1);
+    const float4 b00 = __ldg(p.fam_b + r0 + tc.i0), b01 = __ldg(p.fam_b + r0 + tc.i1);
+    const float4 b10 = __ldg(p.fam_b + r1 + tc.i0), b11 = __ldg(p.fam_b + r1 + tc.i1);
+    f.A.x = tsb_lerp4(a00.x, a01.x, a10.x, a11.x, tc.fs, tc.ft);
+    f.A.y = tsb_lerp4(a00.y, a01.y, a10.y, a11.y, tc.fs, tc.ft);
+    f.A.z = tsb_lerp4(a00.z, a01.z, a10.z, a11.z, tc.fs, tc.ft);
+    f.A.w = tsb_lerp4(a00.w, a01.w, a10.w, a11.w, tc.fs, tc.ft);
+    f.B.x = tsb_lerp4(b00.x, b01.x, b10.x, b11.x, tc.fs, tc.ft);
+    f.B.y = tsb_lerp4(b00.y, b01.y, b10.y, b11.y, tc.fs, tc.ft);
+    f.B.z = tsb_lerp4(b00.z, b01.z, b10.z, b11.z, tc.fs, tc.ft);
+    f.B.w = 0.f;
+  }
 }
 
+// Attribute row x (rasterize.py:261-317 channel order) and composite.
+template <int MODE>
+__device__ __forceinline__ float frag_composite(const MatRec& m, const Frag& f, float* acc,
+                                                float T) {
+  float xa[12];
+  xa[0] = f.A.x; xa[1] = f.A.y; xa[2] = f.A.z;
+  xa[3] = f.B.z;  // metallic
+  xa[4] = f.A.w;  // roughness
+  if (MODE == TSB_MODE_FLAT) {
+    xa[5] = m.frame[6]; xa[6] = m.frame[7]; xa[7] = m.frame[8];
+  } else {
+    tsb_decode_normal(f.B.x, f.B.y, m.frame, xa + 5);
+  }
+  xa[8] = m.l_ind[0]; xa[9] = m.l_ind[1]; xa[10] = m.l_ind[2];
+  xa[11] = f.z;
+  return tsb_composite(acc, xa, f.a, T);
+}
+
+constexpr int kRasterCap = 64;  // texturing window (pairs), 2 per lane
+
+// Warp-private shared memory of the rasterizer.
+struct WarpSmem {
+  GeomRec geom[32];           // staged step: intersection forms + test box
+  MatRec mat[32];             // staged step: frame, SH radiance, chart
+  uint32_t act[32];           // lanes with > r live pairs, per round r
+  int32_t rbase[32];          // first pair index of round r
+  float2 xy[32];              // camera-plane coordinates of the 32 pixels
+  float res[10][kRasterCap];  // textured pair attributes (+ z, alpha)
+  uint16_t pairs[32 * 32];    // (lane << 5) | k, round-robin order
+};
+constexpr size_t kRasterWarpSmem = (sizeof(WarpSmem) + 15) & ~size_t(15);
+
+// A pair whose texel fetch is in flight.
+struct PairFetch {
+  float4 A, B;
+  float z, a;
+  int k;
+};
+
+// Stage 1 of texturing a (pixel, splat) pair: intersection values and the
+// texel fetch issue (tex2DLayered in HW mode, 8 corner loads in verify
+// mode); no use of the fetched data yet, so several pairs overlap.
+template <int MODE>
+__device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem& ws, int q,
+                                           PairFetch& f) {
+  const int k = q & 31;
+  const float2 xy = ws.xy[q >> 5];
+  const GeomRec& g = ws.geom[k];
+  const MatRec& m = ws.mat[k];
+  float u, v;
+  tsb_eval_lin(g.lin, xy.x, xy.y, p.near_f, &u, &v, &f.z, &f.a);
+  f.k = k;
+  if (MODE == TSB_MODE_FLAT) {
+    const float* fl = p.flat + 5 * g.id;
+    f.A = make_float4(__ldg(fl), __ldg(fl + 1), __ldg(fl + 2), __ldg(fl + 4));
+    f.B = make_float4(0.f, 0.f, __ldg(fl + 3), 0.f);
+    return;
+  }
+  tsb_texc tc;
+  tsb_texel_coords(u, v, p.T, &tc);
+  if (MODE == TSB_MODE_HW) {
+    const float sx = m.tex_x + tc.xs + 0.5f;
+    const float sy = m.tex_y + tc.yt + 0.5f;
+#ifdef TSB_PROBE_NOTEX
+    f.A = make_float4(sx * 1e-9f, 0.5f, 0.5f, 0.5f);
+    f.B = make_float4(0.5f, sy * 1e-9f + 0.5f, 0.2f, 0.f);
+#else
+    f.A = tex2DLayered<float4>(p.tex_a, sx, sy, m.page);
+    f.B = tex2DLayered<float4>(p.tex_b, sx, sy, m.page);
+#endif
+  } else {
+    const int r0 = m.lin_off + tc.j0 * p.page_w, r1 = m.lin_off + tc.j1 * p.page_w;
+    const float4 a00 = __ldg(p.fam_a + r0 + tc.i0), a01 = __ldg(p.fam_a + r0 + tc.i1);
+    const float4 a10 = __ldg(p.fam_a + r1 + tc.i0), a11 = __ldg(p.fam_a + r1 + tc.i1);
+    const float4 b00 = __ldg(p.fam_b + r0 + tc.i0), b01 = __ldg(p.fam_b + r0 + tc.i1);
+    const float4 b10 = __ldg(p.fam_b + r1 + tc.i0), b11 = __ldg(p.fam_b + r1 + tc.i1);
+    f.A.x = tsb_lerp4(a00.x, a01.x, a10.x, a11.x, tc.fs, tc.ft);
+    f.A.y = tsb_lerp4(a00.y, a01.y, a10.y, a11.y, tc.fs, tc.ft);
+    f.A.z = tsb_lerp4(a00.z, a01.z, a10.z, a11.z, tc.fs, tc.ft);
+    f.A.w = tsb_lerp4(a00.w, a01.w, a10.w, a11.w, tc.fs, tc.ft);
+    f.B.x = tsb_lerp4(b00.x, b01.x, b10.x, b11.x, tc.fs, tc.ft);
+    f.B.y = tsb_lerp4(b00.y, b01.y, b10.y, b11.y, tc.fs, tc.ft);
+    f.B.z = tsb_lerp4(b00.z, b01.z, b10.z, b11.z, tc.fs, tc.ft);
+    f.B.w = 0.f;
+  }
+}
+
+// Stage 2: normal decode (rasterize.py:313-314) and the pair's attribute
+// row into result slot t.
+template <int MODE>
+__device__ __forceinline__ void pair_finish(WarpSmem& ws, const PairFetch& f, int t) {
+  const MatRec& m = ws.mat[f.k];
+  float nw[3];
+  if (MODE == TSB_MODE_FLAT) {
+    nw[0] = m.frame[6]; nw[1] = m.frame[7]; nw[2] = m.frame[8];
+  } else {
+    tsb_decode_normal(f.B.x, f.B.y, m.frame, nw);
+  }
+  ws.res[0][t] = f.A.x;
+  ws.res[1][t] = f.A.y;
+  ws.res[2][t] = f.A.z;
+  ws.res[3][t] = f.B.z;  // metallic
+  ws.res[4][t] = f.A.w;  // roughness
+  ws.res[5][t] = nw[0];
+  ws.res[6][t] = nw[1];
+  ws.res[7][t] = nw[2];
+  ws.res[8][t] = f.z;
+  ws.res[9][t] = f.a;
+}
+
+// K5. One CTA per TILE x TILE tile; each warp owns 8 x 4 pixel blocks of the
+// tile and walks the tile's draw-ordered list on its own (no CTA barriers; a
+// warp retires as soon as its pixels saturate). Per step of 32 list entries:
+//   stage    the 32 splat records into warp-private shared memory (SoA) and
+//            ballot the ones whose test box (rect ∩ alpha-cut ellipse box)
+//            touches the block;
+//   decide   per pixel, which candidates composite (test box, 6-FMA linear
+//            forms, division-free reject, alpha cut + fp64 guard band) —
+//            a live bitmask; nothing here depends on transmittance;
+//   compact  the live (pixel, splat) pairs into a round-robin list: all
+//            pixels' first live splat, then all second ones, ...;
+//   texture  all lanes texture the list in windows of 64 pairs, two pairs
+//            per lane in flight (fetch + decode are T-independent);
+//   blend    each pixel composites its pairs of the window in draw order
+//            with the reference's T gate (rasterize.py:366-381).
+// The per-pixel decision and blend sequence is exactly the reference's
+// (tsb_math.h); the work split never changes a bit of the result.
 template <int TILE, int MODE>
-__global__ void __launch_bounds__(TILE * TILE) k_raster_fwd(RasterParams p) {
-  constexpr int BLOCK = TILE * TILE;
-  constexpr int BATCH = BLOCK < 256 ? BLOCK : 256;
-  __shared__ GeomRec s_geom[BATCH];
-
+__global__ void __launch_bounds__(TILE * TILE < 256 ? TILE * TILE : 256,
+                                  TILE == 16 ? TSB_RASTER_MINB : 1)
+k_raster_fwd(RasterParams p) {
+  constexpr int THREADS = TILE * TILE < 256 ? TILE * TILE : 256;
+  constexpr int WARPS = THREADS / 32;
+  constexpr int NBLK = TILE * TILE / 32;  // 8 x 4 pixel blocks per tile
+  constexpr int WX = TILE / 8;            // blocks per tile row
+  constexpr int CAP = kRasterCap;
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpSmem& ws = *reinterpret_cast<WarpSmem*>(s_raw + (size_t)warp * kRasterWarpSmem);
+  const uint32_t lt_mask = (1u << lane) - 1u;
   const int tile = blockIdx.x;
-  const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
-  const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
-  const int px = tx * TILE + lx, py = ty * TILE + ly;
-  const bool inside = px < p.W && py < p.H;
-  const double xd = tsb_pixel_x(&p.cam, px), yd = tsb_pixel_y(&p.cam, py);
-  const float x = (float)xd, y = (float)yd;
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
-
-  float acc[13];
-#pragma unroll
-  for (int c = 0; c < 13; ++c) acc[c] = 0.f;
-  float T = 1.f, T_last = 1.f;
-  int n = 0, last = -1;
-  bool done = !inside;
   const float teps = (float)TSB_TRANSMIT_EPS;
 
-  for (int base = start; base < end; base += BATCH) {
-    if (__syncthreads_count(done) == BLOCK) break;
-    const int i = base + (int)threadIdx.x;
-    if (threadIdx.x < BATCH && i < end) s_geom[threadIdx.x] = p.geom[p.evals[i]];
-    __syncthreads();
-    const int cnt = min(BATCH, end - base);
-    if (!done) {
-      for (int j = 0; j < cnt; ++j) {
-        const GeomRec& g = s_geom[j];
-        if (px < g.x0 || px >= g.x1 || py < g.y0 || py >= g.y1) continue;
-        float u, v, z, a;
-        const int r = tsb_intersect_f32(g.m, g.opacity, x, y, p.near_f, &u, &v, &z, &a);
-        if (r == 0) continue;
-        if (r == 2) {
-          const double* m64 = p.m64 + (size_t)kM64Stride * g.id;
-          if (!tsb_live_f64(m64, m64[9], xd, yd, p.cam.near_z)) continue;
+  for (int blk = warp; blk < NBLK; blk += WARPS) {
+    const int bx0 = (tile % p.tiles_x) * TILE + (blk % WX) * 8;
+    const int by0 = (tile / p.tiles_x) * TILE + (blk / WX) * 4;
+    if (bx0 >= p.W || by0 >= p.H) continue;
+    const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
+    const bool inside = px < p.W && py < p.H;
+    const float x = (float)tsb_pixel_x(&p.cam, px), y = (float)tsb_pixel_y(&p.cam, py);
+    const int bx1 = min(bx0 + 8, p.W), by1 = min(by0 + 4, p.H);
+    __syncwarp();
+    ws.xy[lane] = make_float2(x, y);
+
+    float acc[13];
+#pragma unroll
+    for (int c = 0; c < 13; ++c) acc[c] = 0.f;
+    float T = 1.f, T_last = 1.f;
+    int n = 0, last = -1;
+    bool done = !inside;
+
+    for (int base = start; base < end; base += 32) {
+      if (__all_sync(0xffffffffu, done)) break;
+      // ---- stage
+      const int e = base + lane;
+      bool hit = false;
+      __syncwarp();
+      if (e < end) {
+        const int id = __ldg(p.evals + e);
+        const GeomRec g = p.geom[id];
+        ws.geom[lane] = g;
+        ws.mat[lane] = p.mat[id];
+        hit = (int)(g.bx & 0xFFFF) < bx1 && (int)(g.bx >> 16) > bx0 &&
+              (int)(g.by & 0xFFFF) < by1 && (int)(g.by >> 16) > by0;
+      }
+      const uint32_t cand = __ballot_sync(0xffffffffu, hit);
+      __syncwarp();
+      if (!cand) continue;
+      // ---- decide
+      uint32_t live = 0;
+      if (!done) {
+        for (uint32_t m = cand; m; m &= m - 1) {
+          const int k = __ffs(m) - 1;
+          const GeomRec& g = ws.geom[k];
+          if ((unsigned)(px - (int)(g.bx & 0xFFFF)) >= (unsigned)((int)(g.bx >> 16) - (int)(g.bx & 0xFFFF)) ||
+              (unsigned)(py - (int)(g.by & 0xFFFF)) >= (unsigned)((int)(g.by >> 16) - (int)(g.by & 0xFFFF)))
+            continue;
+          int r = tsb_predecide_lin(g.lin, tsb_lin_r2lo(g.lin), x, y, p.near_f);
+          if (r == 2) {
+            float u, v, z, a;
+            r = tsb_eval_lin(g.lin, x, y, p.near_f, &u, &v, &z, &a);
+          }
+          if (r == 2) {
+            const double* m64 = p.m64 + (size_t)kM64Stride * g.id;
+            r = tsb_live_f64(m64, m64[9], tsb_pixel_x(&p.cam, px), tsb_pixel_y(&p.cam, py),
+                             p.cam.near_z);
+          }
+          if (r) live |= 1u << k;
         }
-        float xa[12];
-        fetch_attrs<MODE>(p, g.id, u, v, z, xa);
-        T_last = T;
-        T = tsb_composite(acc, xa, a, T);
-        ++n;
-        last = base + j;
-        if (!(T > teps)) { done = true; break; }
+      }
+      // ---- compact (round-robin)
+      const int cnt = __popc(live);
+      const int maxc = __reduce_max_sync(0xffffffffu, cnt);
+      if (maxc == 0) continue;
+      int total = 0;
+      {
+        uint32_t m = live;
+        for (int r = 0; r < maxc; ++r) {
+          const uint32_t act = __ballot_sync(0xffffffffu, cnt > r);
+          if (lane == 0) { ws.act[r] = act; ws.rbase[r] = total; }
+          if (cnt > r) {
+            ws.pairs[total + __popc(act & lt_mask)] = (uint16_t)((lane << 5) | (__ffs(m) - 1));
+            m &= m - 1;
+          }
+          total += __popc(act);
+        }
+      }
+      __syncwarp();
+      int r_cur = 0;  // next round this lane blends
+      for (int w = 0; w < total; w += CAP) {
+        // ---- texture pairs [w, w + CAP): issue both fetches, then finish
+        {
+          const int t0 = w + lane, t1 = w + lane + 32;
+          const bool v0 = t0 < total, v1 = t1 < total && t1 < w + CAP;
+          PairFetch f0, f1;
+          if (v0) pair_issue<MODE>(p, ws, ws.pairs[t0], f0);
+          if (v1) pair_issue<MODE>(p, ws, ws.pairs[t1], f1);
+          if (v0) pair_finish<MODE>(ws, f0, lane);
+          if (v1) pair_finish<MODE>(ws, f1, lane + 32);
+        }
+        __syncwarp();
+        // ---- blend this lane's pairs that fall in the window, in order
+        if (!done) {
+          while (r_cur < cnt) {
+            const int pos = ws.rbase[r_cur] + __popc(ws.act[r_cur] & lt_mask);
+            if (pos >= w + CAP) break;
+            const int t = pos - w;
+            const int k = ws.pairs[pos] & 31;
+            float xa[12];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) xa[c] = ws.res[c][t];
+            xa[8] = ws.mat[k].l_ind[0]; xa[9] = ws.mat[k].l_ind[1]; xa[10] = ws.mat[k].l_ind[2];
+            xa[11] = ws.res[8][t];
+            const float a = ws.res[9][t];
+            T_last = T;
+            T = tsb_composite(acc, xa, a, T);
+            ++n;
+            last = base + k;
+            ++r_cur;
+            if (!(T > teps)) { done = true; break; }
+          }
+        }
+        __syncwarp();
       }
     }
-  }
-  if (!inside) return;
-  const int HW = p.W * p.H;
-  const int pix = py * p.W + px;
+    if (inside) {
+      const int HW = p.W * p.H;
+      const int pix = py * p.W + px;
 #pragma unroll
-  for (int c = 0; c < 13; ++c) p.gbuf[(size_t)c * HW + pix] = acc[c];
-  p.n_contrib[pix] = n;
-  p.last_entry[pix] = last;
-  p.final_T[pix] = T;
-  p.T_last[pix] = T_last;
+      for (int c = 0; c < 13; ++c) p.gbuf[(size_t)c * HW + pix] = acc[c];
+      p.n_contrib[pix] = n;
+      p.last_entry[pix] = last;
+      p.final_T[pix] = T;
+      p.T_last[pix] = T_last;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -386,11 +602,12 @@ __global__ void k_export_keys(int64_t cap, const uint32_t* __restrict__ ekeys,
   keys[i] = i < total ? (((int64_t)ekeys[i] << 32) | (int64_t)(uint32_t)rank[evals[i]]) : -1;
 }
 
-__global__ void k_export_rects(int32_t P, const GeomRec* __restrict__ geom, int32_t* __restrict__ rects) {
+__global__ void k_export_rects(int32_t P, const uint2* __restrict__ rc, int32_t* __restrict__ rects) {
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= P) return;
-  const GeomRec g = geom[id];
-  rects[4 * id] = g.x0; rects[4 * id + 1] = g.x1; rects[4 * id + 2] = g.y0; rects[4 * id + 3] = g.y1;
+  const uint32_t rx = rc[id].x, ry = rc[id].y;
+  rects[4 * id] = rx & 0xFFFF; rects[4 * id + 1] = rx >> 16;
+  rects[4 * id + 2] = ry & 0xFFFF; rects[4 * id + 3] = ry >> 16;
 }
 
 __global__ void k_f32_to_f16x4(const float4* __restrict__ src, ushort4* __restrict__ dst, size_t n) {
@@ -421,14 +638,26 @@ __global__ void k_tex_probe(cudaTextureObject_t tex, int32_t window, int32_t ite
   sink[t] = acc;
 }
 
+template <int TILE, int MODE>
+inline cudaError_t launch_raster_mode(int blocks, cudaStream_t st, const RasterParams& rp) {
+  constexpr int threads = TILE * TILE < 256 ? TILE * TILE : 256;
+  const size_t smem = (size_t)(threads / 32) * kRasterWarpSmem;
+  static bool configured = false;  // per instantiation; attribute is per function
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_raster_fwd<TILE, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_raster_fwd<TILE, MODE><<<blocks, threads, smem, st>>>(rp);
+  return cudaGetLastError();
+}
+
 template <int TILE>
-inline void launch_raster(int mode, int blocks, cudaStream_t st, const RasterParams& rp) {
-  if (mode == TSB_MODE_HW)
-    k_raster_fwd<TILE, TSB_MODE_HW><<<blocks, TILE * TILE, 0, st>>>(rp);
-  else if (mode == TSB_MODE_VERIFY)
-    k_raster_fwd<TILE, TSB_MODE_VERIFY><<<blocks, TILE * TILE, 0, st>>>(rp);
-  else
-    k_raster_fwd<TILE, TSB_MODE_FLAT><<<blocks, TILE * TILE, 0, st>>>(rp);
+inline cudaError_t launch_raster(int mode, int blocks, cudaStream_t st, const RasterParams& rp) {
+  if (mode == TSB_MODE_HW) return launch_raster_mode<TILE, TSB_MODE_HW>(blocks, st, rp);
+  if (mode == TSB_MODE_VERIFY) return launch_raster_mode<TILE, TSB_MODE_VERIFY>(blocks, st, rp);
+  return launch_raster_mode<TILE, TSB_MODE_FLAT>(blocks, st, rp);
 }
 
 }  // namespace tsb
@@ -536,7 +765,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     pp.sc = scene->scales; pp.op = scene->opacities; pp.sh = scene->sh;
     pp.entries = mode == TSB_MODE_FLAT ? nullptr : atlas->entries;
     pp.T = atlas->resolution; pp.page_w = atlas->page_w; pp.page_h = atlas->page_h;
-    pp.geom = geom; pp.mat = mat; pp.m64 = m64; pp.dkeys = dk_in; pp.ids = ids_in;
+    pp.geom = geom; pp.rects = ws_ptr<uint2>(ws, L.rects); pp.mat = mat; pp.m64 = m64; pp.dkeys = dk_in; pp.ids = ids_in;
     pp.tile_count = tcount;
     k_preprocess<<<(P + 255) / 256, 256, 0, st>>>(pp);
     TSB_CHECK_LAUNCH("k_preprocess");
@@ -550,7 +779,8 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     const int64_t C = std::max<int64_t>(cap, 1);
     TSB_CUDA(cudaMemsetAsync(ek_in, 0xFF, (size_t)C * 4, st));
     k_duplicate<<<(P + 255) / 256, 256, 0, st>>>(P, tile, L.tiles_x, cap, ids_out, csorted,
-                                                 offsets, geom, ek_in, ev_in, counters);
+                                                 offsets, ws_ptr<uint2>(ws, L.rects), ek_in,
+                                                 ev_in, counters);
     TSB_CHECK_LAUNCH("k_duplicate");
     cub_bytes = L.cub_bytes;
     TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, ek_in, ek_out, ev_in, ev_out,
@@ -591,10 +821,11 @@ int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera, const
   rp.tex_b = atlas->tex ? reinterpret_cast<AtlasTex*>(atlas->tex)->tex_b : 0;
   rp.gbuf = gbuf; rp.n_contrib = px->n_contrib; rp.last_entry = px->last_entry;
   rp.final_T = px->final_T; rp.T_last = px->T_last;
-  if (tile == 8) launch_raster<8>(mode, L.num_tiles, st, rp);
-  else if (tile == 16) launch_raster<16>(mode, L.num_tiles, st, rp);
-  else launch_raster<32>(mode, L.num_tiles, st, rp);
-  TSB_CHECK_LAUNCH("k_raster_fwd");
+  cudaError_t e;
+  if (tile == 8) e = launch_raster<8>(mode, L.num_tiles, st, rp);
+  else if (tile == 16) e = launch_raster<16>(mode, L.num_tiles, st, rp);
+  else e = launch_raster<32>(mode, L.num_tiles, st, rp);
+  if (e != cudaSuccess) return cuda_fail("k_raster_fwd", e);
   return TSB_OK;
 }
 
@@ -635,7 +866,7 @@ int tsb_frame_export(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap,
     TSB_CHECK_LAUNCH("k_export_keys");
   }
   if (rects && P > 0) {
-    k_export_rects<<<(P + 255) / 256, 256, 0, st>>>(P, ws_ptr<GeomRec>(ws, L.geom), rects);
+    k_export_rects<<<(P + 255) / 256, 256, 0, st>>>(P, ws_ptr<uint2>(ws, L.rects), rects);
     TSB_CHECK_LAUNCH("k_export_rects");
   }
   return TSB_OK;

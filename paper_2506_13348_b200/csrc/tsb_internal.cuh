@@ -14,11 +14,13 @@
 namespace tsb {
 
 // Per-splat geometry record staged in shared memory by the rasterizer:
-// fp32 M (rows 0,1,2 x cols 0,1,3), opacity, pixel rect and splat id. 64 B.
+// the linear intersection forms (tsb_make_lin: D, Nu, Nv coefficients,
+// det(M), opacity, reject bound), the pixel test box = reference rect
+// intersected with the alpha-cut ellipse box (tsb_test_box), packed as
+// 16-bit pairs (x0 | x1 << 16, y0 | y1 << 16), and the splat id. 64 B.
 struct __align__(16) GeomRec {
-  float m[9];
-  float opacity;
-  int32_t x0, x1, y0, y1;
+  float lin[TSB_LIN_WORDS];
+  uint32_t bx, by;
   int32_t id;
   int32_t pad;
 };
@@ -46,7 +48,7 @@ struct AtlasTex {
 
 // Workspace carve-up; every offset is 256-B aligned.
 struct WsLayout {
-  size_t geom, mat, m64, dkeys_in, dkeys_out, ids_in, ids_out, tile_count,
+  size_t geom, rects, mat, m64, dkeys_in, dkeys_out, ids_in, ids_out, tile_count,
       counts_sorted, offsets, rank, ekeys_in, ekeys_out, evals_in, evals_out,
       ranges, counters, cub_tmp;
   size_t cub_bytes;
