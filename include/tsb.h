@@ -75,6 +75,9 @@ typedef struct tsb_atlas {
   const float* family_b;       /* same layout (VERIFY) */
   const float* flat_attrs;     /* P x 5: mean albedo rgb, metallic, roughness (FLAT) */
   tsb_atlas_tex_t tex;         /* from tsb_atlas_tex_create (HW), may be NULL otherwise */
+  int32_t texel_stride;        /* float4s between consecutive texels of a family: 1 for
+                                  separate family pages, 2 when A and B are interleaved
+                                  per texel (family_b = family_a + 4 floats) */
 } tsb_atlas;
 
 /* environment.py:209-224 EnvironmentLight + BrdfLut (device, float32). */
@@ -163,6 +166,51 @@ int tsb_atlas_tex_destroy(tsb_atlas_tex_t tex);
  * Writes a checksum per thread into sink (grid*block floats). */
 int tsb_tex_probe(tsb_atlas_tex_t tex, int32_t window, int32_t iters, float* sink,
                   int32_t blocks, int32_t threads, void* stream);
+
+/* ---- Training backward (tsb_backward.cu) ---------------------------------- */
+
+/* Gradient outputs. Scene parameter gradients are float64 like the
+ * parameters (rasterize.py:441-451 SceneGrads); texel gradients are float32
+ * in the reference's per-splat combined layout P x T x T x 7
+ * (albedo.rgb, roughness, metallic, normal a, b). Accumulated into: the
+ * caller zeroes them. */
+typedef struct tsb_scene_grads {
+  double* positions;   /* P x 3 */
+  double* tangent_u;   /* P x 3 */
+  double* tangent_v;   /* P x 3 */
+  double* scales;      /* P x 2 */
+  double* opacities;   /* P     */
+  double* sh;          /* P x K x 3 */
+  float* texels;       /* P x T x T x 7 */
+} tsb_scene_grads;
+
+/* environment.py:198-206 EnvGrads, float32, accumulated into. */
+typedef struct tsb_env_grads {
+  float* spec_mips[TSB_ENV_MAX_LEVELS];
+  float* diffuse;
+} tsb_env_grads;
+
+/* Per-splat scratch bytes needed by tsb_render_backward. */
+int tsb_backward_scratch_size(int32_t num_splats, uint64_t* bytes);
+
+/* K7: adjoint of tsb_shade_forward (replaces shading.shade_backward
+ * shading.py:186-228). dcolor H x W x 3; writes every channel of the planar
+ * dgbuf (13 x H x W) and scatters environment gradients (may be NULL). */
+int tsb_shade_backward(const float* gbuf, const tsb_camera* camera,
+                       const tsb_environment* env, const float* background,
+                       const float* dcolor, float* dgbuf, tsb_env_grads* env_grads,
+                       void* stream);
+
+/* K8 + K9: adjoint of the forward frame left in `workspace` by
+ * tsb_render_forward in TSB_MODE_VERIFY (replaces rasterize.splat_backward
+ * rasterize.py:472-593 and _finish_param_grads :642-676). dgbuf: planar
+ * 13 x H x W gradient of the G-buffer; scratch: tsb_backward_scratch_size
+ * bytes. Gradients are accumulated into `grads`. */
+int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera,
+                        const tsb_atlas* atlas, int32_t tile, const void* workspace,
+                        uint64_t workspace_bytes, int64_t max_entries,
+                        const tsb_pixel_state* pixels, const float* dgbuf, void* scratch,
+                        tsb_scene_grads* grads, void* stream);
 
 /* Last error message of the calling thread. */
 const char* tsb_last_error(void);

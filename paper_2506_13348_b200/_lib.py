@@ -46,7 +46,8 @@ class Scene_t(C.Structure):
 class Atlas_t(C.Structure):
     _fields_ = [("resolution", C.c_int32), ("page_w", C.c_int32), ("page_h", C.c_int32),
                 ("pages", C.c_int32), ("entries", C.c_void_p), ("family_a", C.c_void_p),
-                ("family_b", C.c_void_p), ("flat_attrs", C.c_void_p), ("tex", C.c_void_p)]
+                ("family_b", C.c_void_p), ("flat_attrs", C.c_void_p), ("tex", C.c_void_p),
+                ("texel_stride", C.c_int32)]
 
 
 class Environment_t(C.Structure):
@@ -93,8 +94,8 @@ _SIGNATURES = {
     "tsb_shade_backward": [_P, C.POINTER(Camera_t), C.POINTER(Environment_t), _P, _P, _P,
                            C.POINTER(EnvGrads_t), _P],
     "tsb_render_backward": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
-                            C.c_int32, _P, C.c_uint64, C.c_int64, _P,
-                            C.POINTER(PixelState_t), _P, C.POINTER(SceneGrads_t), _P, _P],
+                            C.c_int32, _P, C.c_uint64, C.c_int64, C.POINTER(PixelState_t), _P,
+                            _P, C.POINTER(SceneGrads_t), _P],
     "tsb_backward_scratch_size": [C.c_int32, C.c_int32, C.POINTER(C.c_uint64)],
 }
 

@@ -231,7 +231,7 @@ struct RasterParams {
   const MatRec* mat;
   const double* m64;
   // texture sources
-  int32_t T, page_w;
+  int32_t T, page_w, tstride;
   const float4* fam_a;
   const float4* fam_b;
   const float* flat;
@@ -271,11 +271,12 @@ __device__ __forceinline__ void frag_fetch(const RasterParams& p, const MatRec& 
     f.A = tex2DLayered<float4>(p.tex_a, sx, sy, m.page);
     f.B = tex2DLayered<float4>(p.tex_b, sx, sy, m.page);
   } else {
+    const int S = p.tstride;
     const int r0 = m.lin_off + tc.j0 * p.page_w, r1 = m.lin_off + tc.j1 * p.page_w;
-    const float4 a00 = __ldg(p.fam_a + r0 + tc.i0), a01 = __ldg(p.fam_a + r0 + tc.i1);
-    const float4 a10 = __ldg(p.fam_a + r1 + tc.i0), a11 = __ldg(p.fam_a + r1 + tc.i1);
-    const float4 b00 = __ldg(p.fam_b + r0 + tc.i0), b01 = __ldg(p.fam_b + r0 + tc.i1);
-    const float4 b10 = __ldg(p.fam_b + r1 + tc.i0), b11 = __ldg(p.fam_b + r1 + tc.i1);
+    const float4 a00 = __ldg(p.fam_a + S * (r0 + tc.i0)), a01 = __ldg(p.fam_a + S * (r0 + tc.i1));
+    const float4 a10 = __ldg(p.fam_a + S * (r1 + tc.i0)), a11 = __ldg(p.fam_a + S * (r1 + tc.i1));
+    const float4 b00 = __ldg(p.fam_b + S * (r0 + tc.i0)), b01 = __ldg(p.fam_b + S * (r0 + tc.i1));
+    const float4 b10 = __ldg(p.fam_b + S * (r1 + tc.i0)), b11 = __ldg(p.fam_b + S * (r1 + tc.i1));
     f.A.x = tsb_lerp4(a00.x, a01.x, a10.x, a11.x, tc.fs, tc.ft);
     f.A.y = tsb_lerp4(a00.y, a01.y, a10.y, a11.y, tc.fs, tc.ft);
     f.A.z = tsb_lerp4(a00.z, a01.z, a10.z, a11.z, tc.fs, tc.ft);
@@ -358,11 +359,12 @@ __device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem
     f.B = tex2DLayered<float4>(p.tex_b, sx, sy, m.page);
 #endif
   } else {
+    const int S = p.tstride;
     const int r0 = m.lin_off + tc.j0 * p.page_w, r1 = m.lin_off + tc.j1 * p.page_w;
-    const float4 a00 = __ldg(p.fam_a + r0 + tc.i0), a01 = __ldg(p.fam_a + r0 + tc.i1);
-    const float4 a10 = __ldg(p.fam_a + r1 + tc.i0), a11 = __ldg(p.fam_a + r1 + tc.i1);
-    const float4 b00 = __ldg(p.fam_b + r0 + tc.i0), b01 = __ldg(p.fam_b + r0 + tc.i1);
-    const float4 b10 = __ldg(p.fam_b + r1 + tc.i0), b11 = __ldg(p.fam_b + r1 + tc.i1);
+    const float4 a00 = __ldg(p.fam_a + S * (r0 + tc.i0)), a01 = __ldg(p.fam_a + S * (r0 + tc.i1));
+    const float4 a10 = __ldg(p.fam_a + S * (r1 + tc.i0)), a11 = __ldg(p.fam_a + S * (r1 + tc.i1));
+    const float4 b00 = __ldg(p.fam_b + S * (r0 + tc.i0)), b01 = __ldg(p.fam_b + S * (r0 + tc.i1));
+    const float4 b10 = __ldg(p.fam_b + S * (r1 + tc.i0)), b11 = __ldg(p.fam_b + S * (r1 + tc.i1));
     f.A.x = tsb_lerp4(a00.x, a01.x, a10.x, a11.x, tc.fs, tc.ft);
     f.A.y = tsb_lerp4(a00.y, a01.y, a10.y, a11.y, tc.fs, tc.ft);
     f.A.z = tsb_lerp4(a00.z, a01.z, a10.z, a11.z, tc.fs, tc.ft);
@@ -814,6 +816,7 @@ int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera, const
   rp.mat = ws_ptr<MatRec>(ws, L.mat);
   rp.m64 = ws_ptr<double>(ws, L.m64);
   rp.T = atlas->resolution; rp.page_w = atlas->page_w;
+  rp.tstride = atlas->texel_stride > 0 ? atlas->texel_stride : 1;
   rp.fam_a = reinterpret_cast<const float4*>(atlas->family_a);
   rp.fam_b = reinterpret_cast<const float4*>(atlas->family_b);
   rp.flat = atlas->flat_attrs;

@@ -130,6 +130,34 @@ class DeviceAtlas:
             self.flat = torch.from_numpy(np.ascontiguousarray(fl, np.float32)).to(dev)
 
     @staticmethod
+    def interleaved(texels8: torch.Tensor) -> "DeviceAtlas":
+        """Verify-mode atlas over a device tensor (P, T, T, 8) holding, per
+        texel, family A (albedo rgb, roughness) then family B (normal a, b,
+        metallic, 0) — the reference's 8-channel page order
+        (rasterize.py:231-233). Chart k is row k of a single T-wide page,
+        so the tensor can be a live training parameter (no repacking)."""
+        if texels8.dim() != 4 or texels8.shape[-1] != 8 or texels8.dtype != torch.float32:
+            raise ValueError("interleaved texels must be (P, T, T, 8) float32")
+        if not texels8.is_contiguous():
+            raise ValueError("interleaved texels must be contiguous")
+        self = DeviceAtlas.__new__(DeviceAtlas)
+        P, T = int(texels8.shape[0]), int(texels8.shape[1])
+        self.device = texels8.device
+        self.resolution = T
+        self.pages, self.page_h, self.page_w = 1, P * T, T
+        k = torch.arange(P, dtype=torch.int32, device=texels8.device)
+        self.entries = torch.stack([torch.zeros_like(k), k, torch.zeros_like(k)], 1).contiguous()
+        self.num_entries = P
+        self.storage = texels8
+        self.family_a = texels8
+        self.family_b = texels8.view(-1)[4:]
+        self.texel_stride = 2
+        self.texel_format = None
+        self.tex = None
+        self.flat = None
+        return self
+
+    @staticmethod
     def flat_only(texels, device=None) -> "DeviceAtlas":
         self = DeviceAtlas.__new__(DeviceAtlas)
         dev = _dev(device)
@@ -153,6 +181,7 @@ class DeviceAtlas:
         a.family_b = _lib.ptr(self.family_b)
         a.flat_attrs = _lib.ptr(self.flat)
         a.tex = self.tex.value if self.tex is not None else None
+        a.texel_stride = getattr(self, "texel_stride", 1)
         return a
 
     def close(self):

@@ -191,6 +191,32 @@ def main():
     np.savez_compressed(OUT / "backward.npz", **d)
     print(f"backward {time.time() - t0:.1f}s", flush=True)
 
+    # ---- compute_step (training.py:130-184) --------------------------------
+    from texsplat.losses import linear_to_display
+    from texsplat.training import compute_step
+    truth = make_gradcheck_scene(seed=11)
+    ct = camera_ring(1, width=32, height=32)[0]
+    gt = render_forward(truth, ct)
+    target = linear_to_display(shade_gbuffer(gt, ct, truth.environment, lut,
+                                             background=truth.background).color)
+    init = truth.copy()
+    init.positions = init.positions + 0.003
+    metrics, gr, eg = compute_step(init, ct, target, lut)
+    d = {}
+    d.update(scene_dict("st_", init))
+    d.update(cam_dict("st_cam_", ct))
+    d["st_target"] = target
+    for k in ("loss", "image", "normal", "smooth", "psnr", "fragments"):
+        d[f"st_m_{k}"] = np.array(metrics[k])
+    for name in ("positions", "tangent_u", "tangent_v", "scales", "opacities", "sh"):
+        d[f"st_g_{name}"] = getattr(gr, name)
+    d["st_g_texels"] = np.stack([t if t is not None else np.zeros((4, 4, 7)) for t in gr.texels])
+    for i, m in enumerate(eg.spec_mips):
+        d[f"st_genv_mip{i}"] = m
+    d["st_genv_diffuse"] = eg.diffuse
+    np.savez_compressed(OUT / "train.npz", **d)
+    print(f"train {time.time() - t0:.1f}s", flush=True)
+
     # ---- cfg2 crop ---------------------------------------------------------
     shell = make_shell_scene(100_000, 8, seed=3)
     shell.environment = _lobe_environment(np.random.default_rng(0), height=64, levels=6)
