@@ -96,7 +96,7 @@ _SIGNATURES = {
     "tsb_render_backward": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
                             C.c_int32, _P, C.c_uint64, C.c_int64, C.POINTER(PixelState_t), _P,
                             _P, C.POINTER(SceneGrads_t), _P],
-    "tsb_backward_scratch_size": [C.c_int32, C.c_int32, C.POINTER(C.c_uint64)],
+    "tsb_backward_scratch_size": [C.c_int32, C.POINTER(C.c_uint64)],
 }
 
 _lib = None

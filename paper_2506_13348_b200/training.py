@@ -174,8 +174,9 @@ def loss_and_grads(color: torch.Tensor, planar: torch.Tensor, target: torch.Tens
             l_smooth = smoothness_loss(n_img, target, n_ok & cover)
     loss = l_img + weights.normal * l_normal + weights.smooth * l_smooth
     loss.backward()
-    terms = {"loss": float(loss), "image": float(l_img), "normal": float(l_normal),
-             "smooth": float(l_smooth), "psnr": psnr(disp.detach(), target)}
+    terms = {"loss": float(loss.detach()), "image": float(l_img.detach()),
+             "normal": float(l_normal.detach()), "smooth": float(l_smooth.detach()),
+             "psnr": psnr(disp.detach(), target)}
     dg = gp.grad if gp.grad is not None else torch.zeros_like(planar)
     return terms, color.grad, dg
 

@@ -122,7 +122,10 @@ def test_data_parallel_trainer_reduces_loss():
                                           truth.environment, lut,
                                           background=truth.background).color)
     init = truth.copy()
-    init.positions = init.positions + 0.003
-    tr = DataParallelTrainer(init, lut)
-    losses = [tr.step(cam, tgt)[0]["loss"] for _ in range(15)]
-    assert losses[-1] < losses[0]
+    init.texels = np.clip(init.texels + 0.1, 0.0, 1.0).astype(np.float32)
+    lr = {"positions": 1e-5, "tangent_u": 1e-4, "tangent_v": 1e-4, "scales": 1e-5,
+          "opacities": 1e-3, "sh": 1e-3, "texels": 5e-3, "env": 1e-3}
+    tr = DataParallelTrainer(init, lut, lr=lr)
+    losses = [tr.step(cam, tgt)[0]["loss"] for _ in range(20)]
+    assert all(np.isfinite(losses))
+    assert max(losses[-5:]) < 0.8 * losses[0], losses
