@@ -227,6 +227,39 @@ class TrainState:
     t: int = 0
 
 
+def partition_views(num_views: int, rank: int, world: int) -> list:
+    """Views of one rank: round-robin r, r + N, ...."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return list(range(rank, num_views, world))
+
+
+def allreduce_mean_(flat: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum a flat gradient buffer over the ranks in one collective and divide
+    by the world size (in place). No-op without an initialised group."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+        flat /= dist.get_world_size(group)
+    return flat
+
+
+def flatten(tensors) -> torch.Tensor:
+    """One float32 buffer from a list of tensors (any float dtype)."""
+    return torch.cat([t.reshape(-1).float() for t in tensors])
+
+
+def unflatten(flat: torch.Tensor, like) -> list:
+    if sum(t.numel() for t in like) != flat.numel():
+        raise ValueError("flat buffer size does not match the templates")
+    out, o = [], 0
+    for t in like:
+        n = t.numel()
+        out.append(flat[o:o + n].view(t.shape))
+        o += n
+    return out
+
+
 class DataParallelTrainer:
     """One rank = one GPU = its own views; one NCCL all-reduce per step."""
 
@@ -328,14 +361,9 @@ class DataParallelTrainer:
     def step(self, camera, target):
         """Forward + backward on this rank's view, all-reduce, Adam update.
         Returns (terms, flat gradient buffer after the all-reduce)."""
-        import torch.distributed as dist
         terms, grads, env_grads = self.grads_and_loss(camera, target)
         flat = self._flat_grads(grads, env_grads)
-        world = 1
-        if dist.is_available() and dist.is_initialized():
-            world = dist.get_world_size(self.group)
-            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
-        flat /= world
+        allreduce_mean_(flat, self.group)
         g = self._unflatten(flat)
         self.step_count += 1
         with torch.no_grad():
