@@ -39,6 +39,14 @@ CPU_BASELINE_NOTE = ("C oracle port of texsplat render_forward+shade_gbuffer (fp
                      "the survey host (SURVEY.md §6)")
 
 
+# BASELINE.json configs; cfg2 is the headline workload.
+CONFIGS = {
+    "cfg2": dict(splats=100_000, texture_res=8, width=800, height=800, env_height=64),
+    "cfg3": dict(splats=500_000, texture_res=8, width=1920, height=1080, env_height=64),
+    "cfg5": dict(splats=2_000_000, texture_res=16, width=1920, height=1080, env_height=128),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -52,10 +60,19 @@ def parse():
     ap.add_argument("--sampler", default="hw", choices=["hw", "verify", "flat"])
     ap.add_argument("--texel-format", default="rgba32f", choices=["rgba32f", "rgba16f"])
     ap.add_argument("--tile", type=int, default=16)
+    ap.add_argument("--env-height", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=20)
-    return ap.parse_args()
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS),
+                    help="BASELINE.json config preset (sets splats/texture/size/env)")
+    ap.add_argument("--workload", default="render", choices=["render", "train"])
+    a = ap.parse_args()
+    preset = CONFIGS[a.config]
+    for k, v in preset.items():
+        if getattr(a, k) == ap.get_default(k):
+            setattr(a, k, v)
+    return a
 
 
 def dist_env():
@@ -122,7 +139,8 @@ def cpu_baseline_run(args, frames: int):
     from paper_2506_13348_b200 import synth
     from paper_2506_13348_b200.environment import BrdfLut
 
-    scene = synth.make_shell_scene(args.splats, args.texture_res, seed=3, with_environment=True)
+    scene = synth.make_shell_scene(args.splats, args.texture_res, seed=3, with_environment=True,
+                                   env_height=args.env_height)
     cams = synth.bench_cameras(256, args.width, args.height)
     lut = BrdfLut.build()
     atlas = oracle.pack(scene.texels)
@@ -167,6 +185,57 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_train(args, scene, cams, lut, rank, world, dev):
+    """cfg4: data-parallel training steps (forward + shade + loss + backward +
+    NCCL all-reduce + Adam), each rank on its own views."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_13348_b200 import render_forward, shade_gbuffer
+    from paper_2506_13348_b200.training import (DataParallelTrainer, linear_to_display,
+                                                partition_views)
+    views = [cams[i] for i in partition_views(len(cams), rank, world)]
+    nt = min(len(views), max(1, args.warmup + args.steps))
+    targets = []
+    for cam in views[:nt]:
+        gb = render_forward(scene, cam, "perprim")
+        targets.append(linear_to_display(shade_gbuffer(gb, cam, scene.environment, lut,
+                                                       background=scene.background).color))
+    init = scene.copy()
+    init.positions = init.positions + 0.003
+    tr = DataParallelTrainer(init, lut)
+    for i in range(args.warmup):
+        tr.step(views[i % nt], targets[i % nt])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        terms, _ = tr.step(views[i % nt], targets[i % nt])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ms = float(t.item())
+        print(json.dumps({
+            "metric": "training steps/s (cfg4: 100k textured 2DGS, 800x800, DP over views)",
+            "value": round(world * args.steps / (ms * 1e-3), 3), "unit": "view-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg4 training step", "splats": args.splats,
+                       "texture_res": args.texture_res, "width": args.width,
+                       "height": args.height, "allreduce": "one NCCL all-reduce of the flat "
+                       "fp32 gradient buffer per step"},
+            "last_loss": terms["loss"]}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -189,9 +258,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    scene = synth.make_shell_scene(args.splats, args.texture_res, seed=3, with_environment=True)
+    scene = synth.make_shell_scene(args.splats, args.texture_res, seed=3, with_environment=True,
+                                   env_height=args.env_height)
     cams = synth.bench_cameras(256, args.width, args.height)
     lut = BrdfLut.build()
+    if args.workload == "train":
+        run_train(args, scene, cams, lut, rank, world, dev)
+        return
     texture_mode = "flat" if args.sampler == "flat" else "atlas"
     atlas = pack_atlases(scene) if texture_mode == "atlas" else None
     r = Renderer(scene, atlas, scene.environment, lut, texture_mode=texture_mode,
@@ -333,7 +406,9 @@ def main():
         "steps": K, "warmup": args.warmup, "ms_per_step": round(max_ms / K, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "splats": P, "texture_res": T, "width": W,
+        "config": {"workload": WORKLOAD if args.config == "cfg2" else
+                   f"{args.config}: {P} textured 2D Gaussians, {T}x{T} atlas, {W}x{H}",
+                   "splats": P, "texture_res": T, "width": W,
                    "height": H, "sampler": args.sampler, "texel_format": args.texel_format,
                    "tile": args.tile, "views": "bench_cameras(256) orbit, rank r takes r::N",
                    "l2": "flushed between timed steps (256 MB write, outside the events)",

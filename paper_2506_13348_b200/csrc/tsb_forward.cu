@@ -29,7 +29,7 @@
 
 // Minimum resident CTAs per SM requested for the 16x16 rasterizer.
 #ifndef TSB_RASTER_MINB
-#define TSB_RASTER_MINB 2
+#define TSB_RASTER_MINB 3
 #endif
 
 namespace tsb {
@@ -59,9 +59,9 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
 
   // CUB temp storage (size queries only; nothing is launched).
   size_t b_depth = 0, b_scan = 0, b_tile = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b_depth, (const uint64_t*)nullptr,
-                                  (uint64_t*)nullptr, (const int32_t*)nullptr,
-                                  (int32_t*)nullptr, (int)Pn, 0, 64);
+  cub::DeviceRadixSort::SortPairs(nullptr, b_depth, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, (int)Pn, 0, 32);
   cub::DeviceScan::ExclusiveSum(nullptr, b_scan, (const int32_t*)nullptr,
                                 (int32_t*)nullptr, (int)Pn);
   cub::DeviceRadixSort::SortPairs(nullptr, b_tile, (const uint32_t*)nullptr,
@@ -77,6 +77,8 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   L->m64 = take(Pn * kM64Stride * sizeof(double));
   L->dkeys_in = take(Pn * 8);
   L->dkeys_out = take(Pn * 8);
+  L->dk32_in = take(Pn * 4);
+  L->dk32_out = take(Pn * 4);
   L->ids_in = take(Pn * 4);
   L->ids_out = take(Pn * 4);
   L->tile_count = take(Pn * 4);
@@ -113,6 +115,8 @@ struct PrepParams {
   MatRec* mat;
   double* m64;
   uint64_t* dkeys;
+  uint32_t* dkey32;
+  uint64_t near_bits;
   int32_t* ids;
   int32_t* tile_count;
 };
@@ -165,9 +169,47 @@ __global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
   for (int k = 0; k < 9; ++k) m64[k] = r.m[k];
   m64[9] = op;
 
-  p.dkeys[id] = r.keep ? tsb_f64_bits(r.view_z) : ~0ull;
+  // 32-bit sort key: (bits(z) - bits(near)) >> 24 is monotone in z for
+  // z > near (positive doubles order like their bit patterns); equal keys
+  // (depths within ~4e-9 relative) are re-ordered by k_fix_runs on the full
+  // 64-bit pattern, so the result is the exact (z, id) order.
+  const uint64_t full = tsb_f64_bits(r.view_z);
+  p.dkeys[id] = r.keep ? full : ~0ull;
+  uint64_t k32 = 0xFFFFFFFEull;
+  if (r.keep) {
+    const uint64_t d = (full - p.near_bits) >> 24;
+    k32 = d < 0xFFFFFFFEull ? d : 0xFFFFFFFEull;
+  }
+  p.dkey32[id] = r.keep ? (uint32_t)k32 : 0xFFFFFFFFu;
   p.ids[id] = id;
   p.tile_count[id] = r.keep ? tsb_rect_tile_count(r.x0, r.x1, r.y0, r.y1, p.tile) : 0;
+}
+
+// S1b: runs of equal 32-bit depth keys leave the stable sort in id order;
+// sort each run by (full fp64 key, id) — runs are rare and short for real
+// scenes (one thread per run, insertion sort; already-sorted runs cost one
+// scan). The culled tail (key 0xFFFFFFFF) stays in id order.
+__global__ void k_fix_runs(int32_t P, const uint32_t* __restrict__ k32,
+                           const uint64_t* __restrict__ k64, int32_t* __restrict__ ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P - 1) return;
+  const uint32_t k = k32[i];
+  if (k == 0xFFFFFFFFu || k32[i + 1] != k || (i > 0 && k32[i - 1] == k)) return;
+  int end = i + 1;
+  while (end + 1 < P && k32[end + 1] == k) ++end;
+  for (int a = i + 1; a <= end; ++a) {
+    const int id = ids[a];
+    const uint64_t key = k64[id];
+    int b = a - 1;
+    while (b >= i) {
+      const int ob = ids[b];
+      const uint64_t kb = k64[ob];
+      if (kb < key || (kb == key && ob < id)) break;
+      ids[b + 1] = ob;
+      --b;
+    }
+    ids[b + 1] = id;
+  }
 }
 
 // K2: per draw-order rank: tile count and rank of each id.
@@ -306,7 +348,10 @@ __device__ __forceinline__ float frag_composite(const MatRec& m, const Frag& f, 
   return tsb_composite(acc, xa, f.a, T);
 }
 
-constexpr int kRasterCap = 64;  // texturing window (pairs), 2 per lane
+#ifndef TSB_RASTER_CAP
+#define TSB_RASTER_CAP 32
+#endif
+constexpr int kRasterCap = TSB_RASTER_CAP;  // texturing window (pairs), CAP/32 per lane
 
 // Warp-private shared memory of the rasterizer.
 struct WarpSmem {
@@ -510,15 +555,20 @@ k_raster_fwd(RasterParams p) {
       __syncwarp();
       int r_cur = 0;  // next round this lane blends
       for (int w = 0; w < total; w += CAP) {
-        // ---- texture pairs [w, w + CAP): issue both fetches, then finish
+        // ---- texture pairs [w, w + CAP): issue every fetch, then finish
         {
-          const int t0 = w + lane, t1 = w + lane + 32;
-          const bool v0 = t0 < total, v1 = t1 < total && t1 < w + CAP;
-          PairFetch f0, f1;
-          if (v0) pair_issue<MODE>(p, ws, ws.pairs[t0], f0);
-          if (v1) pair_issue<MODE>(p, ws, ws.pairs[t1], f1);
-          if (v0) pair_finish<MODE>(ws, f0, lane);
-          if (v1) pair_finish<MODE>(ws, f1, lane + 32);
+          constexpr int NP = CAP / 32;
+          PairFetch f[NP];
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            const int t = w + lane + 32 * j;
+            if (t < total) pair_issue<MODE>(p, ws, ws.pairs[t], f[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            const int t = w + lane + 32 * j;
+            if (t < total) pair_finish<MODE>(ws, f[j], lane + 32 * j);
+          }
         }
         __syncwarp();
         // ---- blend this lane's pairs that fall in the window, in order
@@ -768,12 +818,18 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     pp.entries = mode == TSB_MODE_FLAT ? nullptr : atlas->entries;
     pp.T = atlas->resolution; pp.page_w = atlas->page_w; pp.page_h = atlas->page_h;
     pp.geom = geom; pp.rects = ws_ptr<uint2>(ws, L.rects); pp.mat = mat; pp.m64 = m64; pp.dkeys = dk_in; pp.ids = ids_in;
+    pp.dkey32 = ws_ptr<uint32_t>(ws, L.dk32_in);
+    pp.near_bits = tsb_f64_bits(camera->near_z);
     pp.tile_count = tcount;
     k_preprocess<<<(P + 255) / 256, 256, 0, st>>>(pp);
     TSB_CHECK_LAUNCH("k_preprocess");
 
-    TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, dk_in, dk_out, ids_in, ids_out,
-                                             P, 0, 64, st));
+    TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, ws_ptr<uint32_t>(ws, L.dk32_in),
+                                             ws_ptr<uint32_t>(ws, L.dk32_out), ids_in, ids_out,
+                                             P, 0, 32, st));
+    k_fix_runs<<<(P + 255) / 256, 256, 0, st>>>(P, ws_ptr<uint32_t>(ws, L.dk32_out), dk_in,
+                                                ids_out);
+    TSB_CHECK_LAUNCH("k_fix_runs");
     k_rank_counts<<<(P + 255) / 256, 256, 0, st>>>(P, ids_out, tcount, csorted, rank);
     TSB_CHECK_LAUNCH("k_rank_counts");
     cub_bytes = L.cub_bytes;

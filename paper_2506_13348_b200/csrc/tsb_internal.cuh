@@ -48,7 +48,7 @@ struct AtlasTex {
 
 // Workspace carve-up; every offset is 256-B aligned.
 struct WsLayout {
-  size_t geom, rects, mat, m64, dkeys_in, dkeys_out, ids_in, ids_out, tile_count,
+  size_t geom, rects, mat, m64, dkeys_in, dkeys_out, dk32_in, dk32_out, ids_in, ids_out, tile_count,
       counts_sorted, offsets, rank, ekeys_in, ekeys_out, evals_in, evals_out,
       ranges, counters, cub_tmp;
   size_t cub_bytes;
