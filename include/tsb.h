@@ -193,13 +193,20 @@ typedef struct tsb_env_grads {
 /* Per-splat scratch bytes needed by tsb_render_backward. */
 int tsb_backward_scratch_size(int32_t num_splats, uint64_t* bytes);
 
+/* Scratch bytes for the sharded environment-gradient accumulation of
+ * tsb_shade_backward (32 private copies of the env grids). */
+int tsb_shade_backward_scratch_size(const tsb_environment* env, uint64_t* bytes);
+
 /* K7: adjoint of tsb_shade_forward (replaces shading.shade_backward
  * shading.py:186-228). dcolor H x W x 3; writes every channel of the planar
- * dgbuf (13 x H x W) and scatters environment gradients (may be NULL). */
+ * dgbuf (13 x H x W) and accumulates environment gradients into env_grads
+ * (may be NULL). With scratch (>= tsb_shade_backward_scratch_size bytes)
+ * the env atomics go to per-CTA-group shards that are summed at the end;
+ * scratch may be NULL (direct atomics). */
 int tsb_shade_backward(const float* gbuf, const tsb_camera* camera,
                        const tsb_environment* env, const float* background,
                        const float* dcolor, float* dgbuf, tsb_env_grads* env_grads,
-                       void* stream);
+                       void* scratch, uint64_t scratch_bytes, void* stream);
 
 /* K8 + K9: adjoint of the forward frame left in `workspace` by
  * tsb_render_forward in TSB_MODE_VERIFY (replaces rasterize.splat_backward

@@ -92,7 +92,8 @@ _SIGNATURES = {
     "tsb_atlas_tex_destroy": [_P],
     "tsb_tex_probe": [_P, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P],
     "tsb_shade_backward": [_P, C.POINTER(Camera_t), C.POINTER(Environment_t), _P, _P, _P,
-                           C.POINTER(EnvGrads_t), _P],
+                           C.POINTER(EnvGrads_t), _P, C.c_uint64, _P],
+    "tsb_shade_backward_scratch_size": [C.POINTER(Environment_t), C.POINTER(C.c_uint64)],
     "tsb_render_backward": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
                             C.c_int32, _P, C.c_uint64, C.c_int64, C.POINTER(PixelState_t), _P,
                             _P, C.POINTER(SceneGrads_t), _P],

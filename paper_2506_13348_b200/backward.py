@@ -152,7 +152,16 @@ def shade_backward(result: ShadeResult, camera, env, lut, dcolor):
     cam = _lib.camera_struct(camera)
     es = denv.struct()
     egs = eg.struct()
-    _lib.check(_lib.lib().tsb_shade_backward(_lib.ptr(planar), C.byref(cam), C.byref(es), bgc,
-                                             _lib.ptr(dc), _lib.ptr(dgbuf), C.byref(egs),
-                                             _lib.stream_handle()), "tsb_shade_backward")
+    L = _lib.lib()
+    nb = C.c_uint64()
+    _lib.check(L.tsb_shade_backward_scratch_size(C.byref(es), C.byref(nb)),
+               "tsb_shade_backward_scratch_size")
+    scratch = getattr(denv, "_bwd_scratch", None)
+    if scratch is None or scratch.numel() < nb.value:
+        scratch = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
+        denv._bwd_scratch = scratch
+    _lib.check(L.tsb_shade_backward(_lib.ptr(planar), C.byref(cam), C.byref(es), bgc,
+                                    _lib.ptr(dc), _lib.ptr(dgbuf), C.byref(egs),
+                                    _lib.ptr(scratch), int(scratch.numel()),
+                                    _lib.stream_handle()), "tsb_shade_backward")
     return dgbuf, eg

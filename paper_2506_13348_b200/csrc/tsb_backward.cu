@@ -35,6 +35,23 @@ constexpr int kAccWords = 24;  // per-splat accumulator stride (22 used)
 // accumulator layout: [0..9) dWH rows 0..2 x cols (0,1,3); [9] dopacity;
 // [10..13) dl_ind; [13..16) dframe_u; [16..19) dframe_v; [19..22) dn3.
 
+// Reduce 32 per-lane values across the warp with a transpose butterfly:
+// at each level a lane keeps one half of its vector and sends the other half
+// to its partner, so after 31 shuffles lane l holds the warp total of v[l].
+__device__ __forceinline__ float warp_transpose_reduce(float (&v)[32], int lane) {
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = up ? v[i] : v[i + h];
+      const float keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0];
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -51,9 +68,12 @@ struct ShadeBwdParams {
   const float* gbuf;
   const float* dcolor;  // H x W x 3
   float* dgbuf;         // 13 x H x W
-  float* gmips[TSB_MAX_LEVELS];
+  float* gmips[TSB_MAX_LEVELS];  // shard 0 base of each level (shards contiguous)
   float* gdiffuse;
+  int32_t shard_stride;          // floats between shards (0: no sharding)
 };
+
+constexpr int kEnvShards = 32;
 
 // Bilinear equirect lookup with its taps (environment.py:57-91).
 struct EqTaps {
@@ -124,6 +144,8 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
   const int W = p.cam.width, H = p.cam.height;
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= W * H) return;
+  // this CTA's private copy of the environment gradient grids
+  const size_t shard = p.shard_stride ? (size_t)(blockIdx.x % kEnvShards) * p.shard_stride : 0;
   const size_t HW = (size_t)W * H;
   float g[13];
 #pragma unroll
@@ -193,7 +215,8 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
       dmetal += df0 * (alb[c] - 0.04f);
     }
     float dn_diff[3];
-    eq_grad(env.diffuse, p.gdiffuse, n[0], n[1], n[2], dirr, dn_diff);
+    eq_grad(env.diffuse, p.gdiffuse ? p.gdiffuse + shard : nullptr, n[0], n[1], n[2], dirr,
+            dn_diff);
     // LUT adjoint (environment.py:449-464)
     float dcos_cl, drough_lut;
     {
@@ -226,11 +249,13 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
       float up[3], dd[3];
       const float w0 = l1 != l0 ? 1.0f - fl : (1.0f - fl) + fl;
       for (int c = 0; c < 3; ++c) up[c] = dspec[c] * w0;
-      eq_grad(env.mips[l0], p.gmips[l0], wr[0], wr[1], wr[2], up, dd);
+      eq_grad(env.mips[l0], p.gmips[l0] ? p.gmips[l0] + shard : nullptr, wr[0], wr[1], wr[2],
+              up, dd);
       for (int c = 0; c < 3; ++c) dwr[c] += dd[c];
       if (l1 != l0 && fl != 0.0f) {
         for (int c = 0; c < 3; ++c) up[c] = dspec[c] * fl;
-        eq_grad(env.mips[l1], p.gmips[l1], wr[0], wr[1], wr[2], up, dd);
+        eq_grad(env.mips[l1], p.gmips[l1] ? p.gmips[l1] + shard : nullptr, wr[0], wr[1],
+                wr[2], up, dd);
         for (int c = 0; c < 3; ++c) dwr[c] += dd[c];
       }
     }
@@ -261,6 +286,25 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
   }
 #pragma unroll
   for (int c = 0; c < 13; ++c) p.dgbuf[c * HW + pix] = dg[c];
+}
+
+// Sum the environment-gradient shards into the caller's grids.
+struct EnvShardPlan {
+  float* dst[TSB_MAX_LEVELS + 1];   // caller grids: mips then diffuse
+  int32_t off[TSB_MAX_LEVELS + 2];  // float offset of each grid in a shard
+  int32_t nseg;
+};
+
+__global__ void k_env_shard_reduce(const float* __restrict__ shards, int32_t stride,
+                                   EnvShardPlan plan) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= stride) return;
+  float s = 0.f;
+  for (int k = 0; k < kEnvShards; ++k) s += shards[(size_t)k * stride + i];
+  int seg = 0;
+  while (seg + 1 < plan.nseg && plan.off[seg + 1] <= i) ++seg;
+  float* d = plan.dst[seg];
+  if (d) d[i - plan.off[seg]] += s;
 }
 
 // ---------------------------------------------------------------------------
@@ -376,9 +420,13 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
           }
         }
         if (!__any_sync(0xffffffffu, live)) continue;
-        float c_acc[22];
+        float c_acc[32];
 #pragma unroll
-        for (int c = 0; c < 22; ++c) c_acc[c] = 0.f;
+        for (int c = 0; c < 32; ++c) c_acc[c] = 0.f;
+        int tx_key = -1;
+        float tx_fs = 0.f, tx_ft = 0.f, tx_up[7];
+#pragma unroll
+        for (int c = 0; c < 7; ++c) tx_up[c] = 0.f;
         const MatRec& m = ws.mat[k];
         if (live) {
           // ---- recompute the fragment's attributes (verify sampler)
@@ -446,21 +494,14 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
           float denc[2];
           decode_grad(t7[5], t7[6], gx, gy, gz, denc);
           const float up7[7] = {dx[0], dx[1], dx[2], dx[4], dx[3], denc[0], denc[1]};
-          // ---- texel gradients (per-splat (T, T, 7) combined layout)
-          const float w00 = (1.0f - tc.fs) * (1.0f - tc.ft), w01 = tc.fs * (1.0f - tc.ft);
-          const float w10 = (1.0f - tc.fs) * tc.ft, w11 = tc.fs * tc.ft;
-          float* dt = p.dtexels + (size_t)gr.id * T * T * 7;
-          float* d00 = dt + 7 * (tc.j0 * T + tc.i0);
-          float* d01 = dt + 7 * (tc.j0 * T + tc.i1);
-          float* d10 = dt + 7 * (tc.j1 * T + tc.i0);
-          float* d11 = dt + 7 * (tc.j1 * T + tc.i1);
+          // ---- texel gradients: kept per lane, scattered below per cell group
+          tx_key = tc.j0 * T + tc.i0;
+          tx_fs = tc.fs; tx_ft = tc.ft;
+#pragma unroll
+          for (int c = 0; c < 7; ++c) tx_up[c] = up7[c];
           float dfs = 0.f, dft = 0.f;
 #pragma unroll
           for (int c = 0; c < 7; ++c) {
-            atomicAdd(d00 + c, up7[c] * w00);
-            atomicAdd(d01 + c, up7[c] * w01);
-            atomicAdd(d10 + c, up7[c] * w10);
-            atomicAdd(d11 + c, up7[c] * w11);
             dfs += up7[c] * ((1.0f - tc.ft) * (c01[c] - c00[c]) + tc.ft * (c11[c] - c10[c]));
             dft += up7[c] * ((c10[c] - c00[c]) + tc.fs * ((c11[c] - c10[c]) - (c01[c] - c00[c])));
           }
@@ -500,12 +541,41 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
             c_acc[8] = dz + (x * dhu3 + y * dhv3);
           }
         }
-        // ---- warp-reduce the per-splat terms, one atomic each
-        float* acc = p.acc + (size_t)kAccWords * gr.id;
+        // ---- warp-reduce the 22 per-splat terms (lane c ends with term c)
+        const float tot = warp_transpose_reduce(c_acc, lane);
+        if (lane < 22 && tot != 0.0f) atomicAdd(p.acc + (size_t)kAccWords * gr.id + lane, tot);
+        // ---- texel gradients (per-splat (T, T, 7) combined layout,
+        // rasterize.py:548-562): lanes hitting the same bilinear cell are
+        // reduced together (28 values: 4 corners x 7 channels), one
+        // 28-lane atomic per cell group
+        {
+          float* dt = p.dtexels + (size_t)gr.id * T * T * 7;
+          uint32_t pending = __ballot_sync(0xffffffffu, tx_key >= 0);
+          while (pending) {
+            const int key = __shfl_sync(0xffffffffu, tx_key, __ffs(pending) - 1);
+            const bool in = tx_key == key;
+            pending &= ~__ballot_sync(0xffffffffu, in);
+            float v[32];
+            const float w00 = (1.0f - tx_fs) * (1.0f - tx_ft), w01 = tx_fs * (1.0f - tx_ft);
+            const float w10 = (1.0f - tx_fs) * tx_ft, w11 = tx_fs * tx_ft;
 #pragma unroll
-        for (int c = 0; c < 22; ++c) {
-          const float s = warp_sum(c_acc[c]);
-          if (lane == 0 && s != 0.0f) atomicAdd(acc + c, s);
+            for (int c = 0; c < 7; ++c) {
+              v[c] = in ? tx_up[c] * w00 : 0.f;
+              v[7 + c] = in ? tx_up[c] * w01 : 0.f;
+              v[14 + c] = in ? tx_up[c] * w10 : 0.f;
+              v[21 + c] = in ? tx_up[c] * w11 : 0.f;
+            }
+            v[28] = v[29] = v[30] = v[31] = 0.f;
+            const float tsum = warp_transpose_reduce(v, lane);
+            if (lane < 28) {
+              const int i0 = key % T, j0 = key / T;
+              const int i1 = i0 + 1 < T - 1 ? i0 + 1 : T - 1;
+              const int j1 = j0 + 1 < T - 1 ? j0 + 1 : T - 1;
+              const int corner = lane / 7, ch = lane % 7;
+              const int ii = (corner & 1) ? i1 : i0, jj = (corner & 2) ? j1 : j0;
+              if (tsum != 0.0f) atomicAdd(dt + 7 * (jj * T + ii) + ch, tsum);
+            }
+          }
         }
       }
     }
@@ -675,9 +745,31 @@ int tsb_backward_scratch_size(int32_t P, uint64_t* bytes) {
   return TSB_OK;
 }
 
+static int32_t env_floats(const tsb_environment* env, int32_t* off) {
+  int32_t o = 0;
+  for (int l = 0; l < env->levels; ++l) {
+    if (off) off[l] = o;
+    o += env->mip_h[l] * env->mip_w[l] * 3;
+  }
+  if (off) off[env->levels] = o;
+  o += env->diff_h * env->diff_w * 3;
+  if (off) off[env->levels + 1] = o;
+  return o;
+}
+
+int tsb_shade_backward_scratch_size(const tsb_environment* env, uint64_t* bytes) {
+  if (!env || !bytes || env->levels < 1 || env->levels > TSB_ENV_MAX_LEVELS) {
+    set_error("tsb_shade_backward_scratch_size: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  *bytes = (uint64_t)kEnvShards * env_floats(env, nullptr) * sizeof(float);
+  return TSB_OK;
+}
+
 int tsb_shade_backward(const float* gbuf, const tsb_camera* camera, const tsb_environment* env,
                        const float* background, const float* dcolor, float* dgbuf,
-                       tsb_env_grads* env_grads, void* stream) {
+                       tsb_env_grads* env_grads, void* scratch, uint64_t scratch_bytes,
+                       void* stream) {
   if (!gbuf || !camera || !env || !dcolor || !dgbuf) {
     set_error("tsb_shade_backward: null argument");
     return TSB_ERR_VALUE;
@@ -686,27 +778,44 @@ int tsb_shade_backward(const float* gbuf, const tsb_camera* camera, const tsb_en
     set_error("tsb_shade_backward: bad environment");
     return TSB_ERR_VALUE;
   }
+  cudaStream_t st = (cudaStream_t)stream;
+  EnvShardPlan plan;
+  const int32_t nfl = env_floats(env, plan.off);
+  const bool sharded = env_grads && scratch &&
+                       scratch_bytes >= (uint64_t)kEnvShards * nfl * sizeof(float);
   ShadeBwdParams sp;
   sp.cam = to_cam(camera);
   sp.env.levels = env->levels;
+  float* sh = static_cast<float*>(scratch);
   for (int l = 0; l < TSB_MAX_LEVELS; ++l) {
     const bool on = l < env->levels;
     sp.env.mips[l].data = on ? env->spec_mips[l] : nullptr;
     sp.env.mips[l].h = on ? env->mip_h[l] : 0;
     sp.env.mips[l].w = on ? env->mip_w[l] : 0;
-    sp.gmips[l] = (on && env_grads) ? env_grads->spec_mips[l] : nullptr;
+    float* caller = (on && env_grads) ? env_grads->spec_mips[l] : nullptr;
+    sp.gmips[l] = sharded && caller ? sh + plan.off[l] : caller;
+    plan.dst[l] = on ? caller : nullptr;
   }
   sp.env.diffuse.data = env->diffuse;
   sp.env.diffuse.h = env->diff_h;
   sp.env.diffuse.w = env->diff_w;
   sp.env.lut = env->lut;
   sp.env.lut_res = env->lut_res;
-  sp.gdiffuse = env_grads ? env_grads->diffuse : nullptr;
+  float* cdiff = env_grads ? env_grads->diffuse : nullptr;
+  sp.gdiffuse = sharded && cdiff ? sh + plan.off[env->levels] : cdiff;
+  plan.dst[env->levels] = cdiff;
+  plan.nseg = env->levels + 1;
+  sp.shard_stride = sharded ? nfl : 0;
   for (int c = 0; c < 3; ++c) sp.bg[c] = background ? background[c] : 0.f;
   sp.gbuf = gbuf; sp.dcolor = dcolor; sp.dgbuf = dgbuf;
+  if (sharded) TSB_CUDA(cudaMemsetAsync(sh, 0, (size_t)kEnvShards * nfl * sizeof(float), st));
   const int n = camera->width * camera->height;
-  k_shade_bwd<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(sp);
+  k_shade_bwd<<<(n + 255) / 256, 256, 0, st>>>(sp);
   TSB_CHECK_LAUNCH("k_shade_bwd");
+  if (sharded) {
+    k_env_shard_reduce<<<(nfl + 255) / 256, 256, 0, st>>>(sh, nfl, plan);
+    TSB_CHECK_LAUNCH("k_env_shard_reduce");
+  }
   return TSB_OK;
 }
 
