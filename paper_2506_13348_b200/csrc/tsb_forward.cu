@@ -348,6 +348,9 @@ __device__ __forceinline__ float frag_composite(const MatRec& m, const Frag& f, 
   return tsb_composite(acc, xa, f.a, T);
 }
 
+#ifndef TSB_DECIDE_ILP
+#define TSB_DECIDE_ILP 2
+#endif
 #ifndef TSB_RASTER_CAP
 #define TSB_RASTER_CAP 32
 #endif
@@ -516,17 +519,32 @@ k_raster_fwd(RasterParams p) {
       // ---- decide
       uint32_t live = 0;
       if (!done) {
-        for (uint32_t m = cand; m; m &= m - 1) {
+        // TSB_DECIDE_ILP candidates per iteration, predicated (independent chains)
+        uint32_t undecided = 0;
+        for (uint32_t m = cand; m;) {
+          int kk[TSB_DECIDE_ILP];
+#pragma unroll
+          for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
+            kk[j] = m ? __ffs(m) - 1 : kk[0];
+            m &= m - 1;
+          }
+#pragma unroll
+          for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
+            const GeomRec& g = ws.geom[kk[j]];
+            const bool in =
+                (unsigned)(px - (int)(g.bx & 0xFFFF)) < (unsigned)((int)(g.bx >> 16) - (int)(g.bx & 0xFFFF)) &&
+                (unsigned)(py - (int)(g.by & 0xFFFF)) < (unsigned)((int)(g.by >> 16) - (int)(g.by & 0xFFFF));
+            const int r = tsb_predecide_lin_nb(g.lin, tsb_lin_r2lo(g.lin), x, y, p.near_f);
+            live |= (in && r == 1 ? 1u : 0u) << kk[j];
+            undecided |= (in && r == 2 ? 1u : 0u) << kk[j];
+          }
+        }
+        // the rare candidates near the alpha cut / near plane: exact path
+        for (uint32_t m = undecided; m; m &= m - 1) {
           const int k = __ffs(m) - 1;
           const GeomRec& g = ws.geom[k];
-          if ((unsigned)(px - (int)(g.bx & 0xFFFF)) >= (unsigned)((int)(g.bx >> 16) - (int)(g.bx & 0xFFFF)) ||
-              (unsigned)(py - (int)(g.by & 0xFFFF)) >= (unsigned)((int)(g.by >> 16) - (int)(g.by & 0xFFFF)))
-            continue;
-          int r = tsb_predecide_lin(g.lin, tsb_lin_r2lo(g.lin), x, y, p.near_f);
-          if (r == 2) {
-            float u, v, z, a;
-            r = tsb_eval_lin(g.lin, x, y, p.near_f, &u, &v, &z, &a);
-          }
+          float u, v, z, a;
+          int r = tsb_eval_lin(g.lin, x, y, p.near_f, &u, &v, &z, &a);
           if (r == 2) {
             const double* m64 = p.m64 + (size_t)kM64Stride * g.id;
             r = tsb_live_f64(m64, m64[9], tsb_pixel_x(&p.cam, px), tsb_pixel_y(&p.cam, py),
