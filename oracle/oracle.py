@@ -61,6 +61,8 @@ def lib():
     h.oracle_frame_export.argtypes = [P, P, P, P, P, P]
     h.oracle_frame_raster.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P, P, P, P,
                                       C.c_int32, P, P, P, P, P]
+    h.oracle_frame_set_binning.argtypes = [P, C.c_int32]
+    h.oracle_frame_entry_stats.argtypes = [P, P, P]
     h.oracle_shade.argtypes = [P, P, C.c_int32, P, P, P, C.c_int32, C.c_int32, P, C.c_int32, P,
                                C.c_int32, P, P, P]
     _lib = h
@@ -126,8 +128,11 @@ def flat_attrs(texels):
     return out
 
 
-def render(scene, cam, mode="verify", tile=16, threads=0, atlas=None):
+def render(scene, cam, mode="verify", tile=16, threads=0, atlas=None, binning="box"):
     """Oracle forward. mode 'verify' (fp32 SW bilinear) or 'flat'.
+    binning: "rect" = the reference's _tile_lists (rasterize.py:246-258),
+    "box" = rect ∩ alpha-cut ellipse box (what the GPU bins with); pixels
+    are identical under both when the box is conservative.
     atlas: optional (fam_a, fam_b, entries) from pack(); packed here if None.
     Returns dict with gbuf (13,H,W) f32, n_contrib, last_entry, final_T,
     T_last (H,W), sorted_ids (P,), keys (E,), ranges (tiles,2), rects (P,4),
@@ -142,6 +147,7 @@ def render(scene, cam, mode="verify", tile=16, threads=0, atlas=None):
     f = L.oracle_frame_new(P, int(scene.sh_degree), *[_p(a) for a in arrs], _p(sh), C.byref(c),
                            tile, threads)
     try:
+        L.oracle_frame_set_binning(f, 1 if binning == "box" else 0)
         E = L.oracle_frame_num_entries(f)
         NT = L.oracle_frame_num_tiles(f)
         sorted_ids = np.empty(max(P, 1), np.int32)

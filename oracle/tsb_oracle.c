@@ -50,11 +50,19 @@ typedef struct oracle_frame {
   double* view_z;      /* P */
   int32_t* keep;       /* P */
   int32_t* rank;       /* P */
+  int32_t* boxes;      /* P x 4 test boxes (rect ∩ alpha-cut ellipse box) */
   /* draw order and tile lists */
   int32_t* sorted_ids; /* P: kept in (z, id) order, then culled in id order */
-  int32_t* ranges;     /* num_tiles x 2 */
-  int32_t* entry_ids;  /* num_entries */
-  int64_t* keys;       /* num_entries: (tile << 32) | rank */
+  /* two binnings: [0] by the reference rect (_tile_lists), [1] by the
+   * test box (the GPU's binning); same draw order within each tile */
+  int64_t n_ent[2];
+  int32_t* ranges_b[2];   /* num_tiles x 2 */
+  int32_t* entry_ids_b[2];
+  int64_t* keys_b[2];     /* (tile << 32) | rank */
+  int binning;            /* which one raster/export use (default 1) */
+  int32_t* ranges;
+  int32_t* entry_ids;
+  int64_t* keys;
 } oracle_frame;
 
 static const double* g_sort_z;
@@ -70,8 +78,19 @@ void oracle_frame_free(oracle_frame* f) {
   if (!f) return;
   free(f->lin); free(f->m64); free(f->rects); free(f->frame);
   free(f->l_ind); free(f->view_z); free(f->keep); free(f->rank); free(f->sorted_ids);
-  free(f->ranges); free(f->entry_ids); free(f->keys);
+  for (int b = 0; b < 2; ++b) { free(f->ranges_b[b]); free(f->entry_ids_b[b]); free(f->keys_b[b]); }
+  free(f->boxes);
   free(f);
+}
+
+/* Select the tile lists raster/export use: 0 = reference rect binning
+ * (rasterize.py:246-258), 1 = test-box binning (the GPU's). */
+void oracle_frame_set_binning(oracle_frame* f, int32_t which) {
+  f->binning = which ? 1 : 0;
+  f->num_entries = f->n_ent[f->binning];
+  f->ranges = f->ranges_b[f->binning];
+  f->entry_ids = f->entry_ids_b[f->binning];
+  f->keys = f->keys_b[f->binning];
 }
 
 /* prepare + sort + binning. cam: tsb_cam_params layout (== tsb_camera). */
@@ -96,7 +115,6 @@ oracle_frame* oracle_frame_new(int32_t P, int32_t sh_degree, const double* posit
   f->keep = (int32_t*)malloc(Pn * sizeof(int32_t));
   f->rank = (int32_t*)malloc(Pn * sizeof(int32_t));
   f->sorted_ids = (int32_t*)malloc(Pn * sizeof(int32_t));
-  f->ranges = (int32_t*)calloc((size_t)f->num_tiles * 2, sizeof(int32_t));
   const int K = (sh_degree + 1) * (sh_degree + 1);
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -129,43 +147,58 @@ oracle_frame* oracle_frame_new(int32_t P, int32_t sh_degree, const double* posit
   for (int32_t id = 0; id < P; ++id) if (!f->keep[id]) f->sorted_ids[c++] = id;
   for (int32_t r = 0; r < P; ++r) f->rank[f->sorted_ids[r]] = r;
 
-  /* stable counting sort of (tile, rank) entries == _tile_lists */
-  int64_t* count = (int64_t*)calloc((size_t)f->num_tiles + 1, sizeof(int64_t));
-  int64_t total = 0;
-  for (int32_t r = 0; r < nk; ++r) {
-    const int32_t* rc = f->rects + 4 * (size_t)f->sorted_ids[r];
-    for (int ty = rc[2] / tile; ty <= (rc[3] - 1) / tile; ++ty)
-      for (int tx = rc[0] / tile; tx <= (rc[1] - 1) / tile; ++tx) {
-        count[ty * f->tiles_x + tx]++;
-        total++;
-      }
-  }
-  f->num_entries = total;
-  int64_t* pos = (int64_t*)malloc(((size_t)f->num_tiles + 1) * sizeof(int64_t));
-  int64_t acc = 0;
-  for (int t = 0; t < f->num_tiles; ++t) {
-    pos[t] = acc;
-    f->ranges[2 * t] = (int32_t)acc;
-    acc += count[t];
-    f->ranges[2 * t + 1] = (int32_t)acc;
-    if (count[t] == 0) { f->ranges[2 * t] = 0; f->ranges[2 * t + 1] = 0; }
-  }
-  size_t Tn = total > 0 ? (size_t)total : 1;
-  f->entry_ids = (int32_t*)malloc(Tn * sizeof(int32_t));
-  f->keys = (int64_t*)malloc(Tn * sizeof(int64_t));
-  for (int32_t r = 0; r < nk; ++r) {
-    const int32_t id = f->sorted_ids[r];
+  /* boxes for the tighter binning (shared tsb_test_box) */
+  f->boxes = (int32_t*)malloc(Pn * 4 * sizeof(int32_t));
+  for (int32_t id = 0; id < P; ++id) {
     const int32_t* rc = f->rects + 4 * (size_t)id;
-    for (int ty = rc[2] / tile; ty <= (rc[3] - 1) / tile; ++ty)
-      for (int tx = rc[0] / tile; tx <= (rc[1] - 1) / tile; ++tx) {
-        int t = ty * f->tiles_x + tx;
-        int64_t o = pos[t]++;
-        f->entry_ids[o] = id;
-        f->keys[o] = ((int64_t)t << 32) | (int64_t)(uint32_t)r;
-      }
+    tsb_test_box(cam, f->m64 + 10 * (size_t)id, f->lin[TSB_LIN_WORDS * (size_t)id + 11], rc[0],
+                 rc[1], rc[2], rc[3], f->boxes + 4 * (size_t)id);
   }
-  free(count);
-  free(pos);
+  for (int bsel = 0; bsel < 2; ++bsel) {
+    const int32_t* bx = bsel == 0 ? f->rects : f->boxes;
+    /* stable counting sort of (tile, rank) entries == _tile_lists */
+    int64_t* count = (int64_t*)calloc((size_t)f->num_tiles + 1, sizeof(int64_t));
+    int64_t total = 0;
+    for (int32_t r = 0; r < nk; ++r) {
+      const int32_t* rc = bx + 4 * (size_t)f->sorted_ids[r];
+      if (!(rc[1] > rc[0] && rc[3] > rc[2])) continue;
+      for (int ty = rc[2] / tile; ty <= (rc[3] - 1) / tile; ++ty)
+        for (int tx = rc[0] / tile; tx <= (rc[1] - 1) / tile; ++tx) {
+          count[ty * f->tiles_x + tx]++;
+          total++;
+        }
+    }
+    f->n_ent[bsel] = total;
+    f->ranges_b[bsel] = (int32_t*)calloc((size_t)f->num_tiles * 2, sizeof(int32_t));
+    int32_t* rg = f->ranges_b[bsel];
+    int64_t* pos = (int64_t*)malloc(((size_t)f->num_tiles + 1) * sizeof(int64_t));
+    int64_t acc = 0;
+    for (int t = 0; t < f->num_tiles; ++t) {
+      pos[t] = acc;
+      rg[2 * t] = (int32_t)acc;
+      acc += count[t];
+      rg[2 * t + 1] = (int32_t)acc;
+      if (count[t] == 0) { rg[2 * t] = 0; rg[2 * t + 1] = 0; }
+    }
+    size_t Tn = total > 0 ? (size_t)total : 1;
+    f->entry_ids_b[bsel] = (int32_t*)malloc(Tn * sizeof(int32_t));
+    f->keys_b[bsel] = (int64_t*)malloc(Tn * sizeof(int64_t));
+    for (int32_t r = 0; r < nk; ++r) {
+      const int32_t id = f->sorted_ids[r];
+      const int32_t* rc = bx + 4 * (size_t)id;
+      if (!(rc[1] > rc[0] && rc[3] > rc[2])) continue;
+      for (int ty = rc[2] / tile; ty <= (rc[3] - 1) / tile; ++ty)
+        for (int tx = rc[0] / tile; tx <= (rc[1] - 1) / tile; ++tx) {
+          int t = ty * f->tiles_x + tx;
+          int64_t o = pos[t]++;
+          f->entry_ids_b[bsel][o] = id;
+          f->keys_b[bsel][o] = ((int64_t)t << 32) | (int64_t)(uint32_t)r;
+        }
+    }
+    free(count);
+    free(pos);
+  }
+  oracle_frame_set_binning(f, 1);
   return f;
 }
 
@@ -330,4 +363,10 @@ void oracle_shade(const float* gbuf, const tsb_cam_params* cam, int32_t levels,
       tsb_shade_pixel(g, wo, &env, bg, color + 3 * pix, dif + 3 * pix, spe + 3 * pix);
     }
   }
+}
+
+/* Entries under both binnings (diagnostics). */
+void oracle_frame_entry_stats(const oracle_frame* f, int64_t* by_rect, int64_t* by_box) {
+  *by_rect = f->n_ent[0];
+  *by_box = f->n_ent[1];
 }

@@ -6,7 +6,8 @@
 //                       order => ties broken by id, == np.lexsort((ids, z)))
 //   K2 k_rank_counts    per rank: tile count, rank of id
 //   S2 exclusive scan   entry offsets in draw order
-//   K3 k_duplicate      (tile, id) entries in draw order
+//   K3 k_duplicate_lb   (tile, id) entries in draw order, binned by the test
+//                       box (rect ∩ alpha-cut ellipse box), load-balanced
 //   S3 tile sort        stable radix sort on tile bits only => per-tile lists
 //                       keep draw order (== keys (tile << 32) | rank)
 //   K4 k_ranges         [start, end) per tile
@@ -182,7 +183,11 @@ __global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
   }
   p.dkey32[id] = r.keep ? (uint32_t)k32 : 0xFFFFFFFFu;
   p.ids[id] = id;
-  p.tile_count[id] = r.keep ? tsb_rect_tile_count(r.x0, r.x1, r.y0, r.y1, p.tile) : 0;
+  // Tile binning by the test box (reference rect ∩ alpha-cut ellipse box):
+  // a strictly tighter, conservative version of _tile_lists' rect binning
+  // (rasterize.py:246-258) — tiles outside it cannot hold a live pixel.
+  const bool box_ok = tb[1] > tb[0] && tb[3] > tb[2];
+  p.tile_count[id] = (r.keep && box_ok) ? tsb_rect_tile_count(tb[0], tb[1], tb[2], tb[3], p.tile) : 0;
 }
 
 // S1b: runs of equal 32-bit depth keys leave the stable sort in id order;
@@ -223,29 +228,68 @@ __global__ void k_rank_counts(int32_t P, const int32_t* __restrict__ sorted_ids,
   rank[id] = r;
 }
 
-// K3: duplicate each splat into every tile its rect touches, in draw order.
-__global__ void k_duplicate(int32_t P, int32_t tile, int32_t tiles_x, int64_t cap,
-                            const int32_t* __restrict__ sorted_ids,
-                            const int32_t* __restrict__ counts_sorted,
-                            const int32_t* __restrict__ offsets,
-                            const uint2* __restrict__ rects, uint32_t* __restrict__ ekeys,
-                            int32_t* __restrict__ evals, int64_t* __restrict__ counters) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P) return;
-  const int cnt = counts_sorted[r];
-  const int64_t off = offsets[r];
-  if (r == P - 1) counters[0] = off + cnt;
-  if (cnt == 0 || off + cnt > cap) return;
-  const int id = sorted_ids[r];
-  const uint2 rc = rects[id];
-  const int x0 = rc.x & 0xFFFF, x1 = rc.x >> 16, y0 = rc.y & 0xFFFF, y1 = rc.y >> 16;
-  int64_t o = off;
-  for (int ty = y0 / tile; ty <= (y1 - 1) / tile; ++ty)
-    for (int tx = x0 / tile; tx <= (x1 - 1) / tile; ++tx) {
-      ekeys[o] = (uint32_t)(ty * tiles_x + tx);
-      evals[o] = id;
-      ++o;
+// K3 (load-balanced): one thread per 4 consecutive output entries. The
+// owning draw-order rank of entry e is the last r with offsets[r] <= e
+// (binary search over the exclusive scan; zero-count ranks are skipped
+// because they share their successor's offset). Entries of a splat follow
+// its rect's tiles row by row, exactly like the per-splat loop above, and
+// each thread stores 4 keys + 4 ids as two 16-B vectors (coalesced).
+__global__ void __launch_bounds__(256) k_duplicate_lb(
+    int32_t P, int32_t tile, int32_t tiles_x, int64_t cap,
+    const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ counts_sorted,
+    const int32_t* __restrict__ offsets, const GeomRec* __restrict__ boxes,
+    uint32_t* __restrict__ ekeys, int32_t* __restrict__ evals, int64_t* __restrict__ counters) {
+  const int64_t e0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const int64_t total = (int64_t)offsets[P - 1] + counts_sorted[P - 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) counters[0] = total;
+  if (e0 >= cap) return;
+  if (total > cap || e0 >= total) {  // padding: sorts after every real tile
+    if (e0 + 4 <= cap) {
+      *reinterpret_cast<uint4*>(ekeys + e0) = make_uint4(~0u, ~0u, ~0u, ~0u);
+    } else {
+      for (int64_t e = e0; e < cap; ++e) ekeys[e] = ~0u;
     }
+    return;
+  }
+  // upper_bound(offsets, e0) - 1
+  int lo = 0, hi = P;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(offsets + mid) <= e0) lo = mid; else hi = mid;
+  }
+  int r = lo, cur = -1;
+  uint32_t kq[4];
+  int32_t vq[4];
+  int id = 0, nxt = 1, ty0 = 0, tx0 = 0, off = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t e = e0 + q;
+    kq[q] = 0xFFFFFFFFu;
+    vq[q] = 0;
+    if (e >= total) continue;
+    // advance to the rank whose [offset, offset + count) holds e (zero-count
+    // ranks are skipped; terminates because e < total)
+    while (e >= (int64_t)__ldg(offsets + r) + __ldg(counts_sorted + r)) ++r;
+    if (r != cur) {
+      cur = r;
+      off = __ldg(offsets + r);
+      id = __ldg(sorted_ids + r);
+      const uint32_t bx = __ldg(&boxes[id].bx), by = __ldg(&boxes[id].by);
+      const int x0 = bx & 0xFFFF, x1 = bx >> 16, y0 = by & 0xFFFF;
+      tx0 = x0 / tile;
+      nxt = (x1 - 1) / tile - tx0 + 1;
+      ty0 = y0 / tile;
+    }
+    const int j = (int)(e - off);
+    kq[q] = (uint32_t)((ty0 + j / nxt) * tiles_x + tx0 + j % nxt);
+    vq[q] = id;
+  }
+  if (e0 + 4 <= cap) {
+    *reinterpret_cast<uint4*>(ekeys + e0) = make_uint4(kq[0], kq[1], kq[2], kq[3]);
+    *reinterpret_cast<int4*>(evals + e0) = make_int4(vq[0], vq[1], vq[2], vq[3]);
+  } else {
+    for (int q = 0; q < 4 && e0 + q < cap; ++q) { ekeys[e0 + q] = kq[q]; evals[e0 + q] = vq[q]; }
+  }
 }
 
 // K4: tile ranges from the tile-sorted entry keys.
@@ -853,11 +897,9 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     cub_bytes = L.cub_bytes;
     TSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, csorted, offsets, P, st));
     const int64_t C = std::max<int64_t>(cap, 1);
-    TSB_CUDA(cudaMemsetAsync(ek_in, 0xFF, (size_t)C * 4, st));
-    k_duplicate<<<(P + 255) / 256, 256, 0, st>>>(P, tile, L.tiles_x, cap, ids_out, csorted,
-                                                 offsets, ws_ptr<uint2>(ws, L.rects), ek_in,
-                                                 ev_in, counters);
-    TSB_CHECK_LAUNCH("k_duplicate");
+    k_duplicate_lb<<<(unsigned)((C + 1023) / 1024), 256, 0, st>>>(
+        P, tile, L.tiles_x, cap, ids_out, csorted, offsets, geom, ek_in, ev_in, counters);
+    TSB_CHECK_LAUNCH("k_duplicate_lb");
     cub_bytes = L.cub_bytes;
     TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, ek_in, ek_out, ev_in, ev_out,
                                              (int)C, 0, L.tile_bits, st));

@@ -233,6 +233,10 @@ def test_cfg2_full_frame_bit_exact_vs_oracle(lut_table):
     _assert_structure_equal(tape, ref)
     _assert_pixels_equal(gb, ref)
     assert np.array_equal(_np(gb.planar), ref["gbuf"])
+    # the reference's rect binning renders the same pixels (box is conservative)
+    ref_rect = oracle.render(scene, cam, tile=16, binning="rect")
+    assert np.array_equal(_np(gb.planar), ref_rect["gbuf"])
+    assert np.array_equal(_np(gb.pixels.n_contrib), ref_rect["n_contrib"])
     full = np.load(gio.GOLDEN / "cfg2_full.npz")
     assert np.abs(_np(gb.alpha) - full["alpha"]).max() <= TOL
     sr = shade_gbuffer(gb, cam, scene.environment, gio.lut(), background=scene.background)

@@ -96,3 +96,23 @@ def test_cfg2_full_frame():
     color, _, _ = oracle.shade(r["gbuf"], cam, scene.environment, gio.load("lut")["table"],
                                scene.background)
     assert np.abs(color - g["color"]).max() <= TOL
+
+
+@pytest.mark.parametrize("case", ["cfg1", "small_inv", "cfg2_crop"])
+def test_box_binning_is_conservative(case):
+    """Binning by rect ∩ alpha-cut ellipse box (the GPU's) renders exactly
+    what the reference's rect binning (_tile_lists) renders."""
+    if case == "cfg1":
+        g = gio.load("cfg1")
+        scene, cam = gio.scene(g), gio.camera(g)
+    elif case == "small_inv":
+        g = gio.load("small")
+        scene, cam = gio.scene(g, "inv_"), gio.camera(g, "inv_cam_")
+    else:
+        g = gio.load("cfg2_crop")
+        scene, cam = gio.cfg2_scene(), gio.camera(g)
+    a = oracle.render(scene, cam, binning="rect")
+    b = oracle.render(scene, cam, binning="box")
+    assert len(b["keys"]) <= len(a["keys"])
+    for k in ("gbuf", "n_contrib", "final_T", "T_last"):
+        assert np.array_equal(a[k], b[k]), k
