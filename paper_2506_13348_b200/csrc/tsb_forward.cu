@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
 
   GeomRec g;
   tsb_make_lin(r.m, op, g.lin);
+  g.r2lo = tsb_lin_r2lo(g.lin);
   p.rects[id] = make_uint2((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
                            (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
   int32_t tb[4];
@@ -148,7 +149,6 @@ __global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
   g.bx = (uint32_t)tb[0] | ((uint32_t)tb[1] << 16);
   g.by = (uint32_t)tb[2] | ((uint32_t)tb[3] << 16);
   g.id = id;
-  g.pad = 0;
   p.geom[id] = g;
 
   MatRec m;
@@ -578,7 +578,7 @@ k_raster_fwd(RasterParams p) {
             const bool in =
                 (unsigned)(px - (int)(g.bx & 0xFFFF)) < (unsigned)((int)(g.bx >> 16) - (int)(g.bx & 0xFFFF)) &&
                 (unsigned)(py - (int)(g.by & 0xFFFF)) < (unsigned)((int)(g.by >> 16) - (int)(g.by & 0xFFFF));
-            const int r = tsb_predecide_lin_nb(g.lin, tsb_lin_r2lo(g.lin), x, y, p.near_f);
+            const int r = tsb_predecide_lin_nb(g.lin, g.r2lo, x, y, p.near_f);
             live |= (in && r == 1 ? 1u : 0u) << kk[j];
             undecided |= (in && r == 2 ? 1u : 0u) << kk[j];
           }

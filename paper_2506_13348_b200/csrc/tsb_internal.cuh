@@ -22,7 +22,7 @@ struct __align__(16) GeomRec {
   float lin[TSB_LIN_WORDS];
   uint32_t bx, by;
   int32_t id;
-  int32_t pad;
+  float r2lo;  // tsb_lin_r2lo(lin): "surely live" bound of the pre-decision
 };
 static_assert(sizeof(GeomRec) == 64, "GeomRec is 64 B");
 
