@@ -97,9 +97,10 @@ __device__ __forceinline__ EqTaps eq_taps(const tsb_grid& g, float dx, float dy,
   const int r0 = (int)r0f;
   const int r1 = r0 + 1 < h - 1 ? r0 + 1 : h - 1;
   const float colf = floorf(col);
-  int c0 = (int)colf % w;
+  int c0 = (int)colf;
   if (c0 < 0) c0 += w;
-  const int c1 = (c0 + 1) % w;
+  if (c0 >= w) c0 -= w;
+  const int c1 = c0 + 1 == w ? 0 : c0 + 1;
   EqTaps t;
   t.i00 = r0 * w + c0; t.i01 = r0 * w + c1; t.i10 = r1 * w + c0; t.i11 = r1 * w + c1;
   t.fr = rowc - r0f; t.fc = col - colf;
@@ -159,8 +160,9 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
     float wo[3];
     tsb_view_dir(&p.cam, tsb_pixel_x(&p.cam, px), tsb_pixel_y(&p.cam, py), wo);
     const tsb_env_params& env = p.env;
-    const float alb[3] = {g[0] / a, g[1] / a, g[2] / a};
-    const float metal = g[3] / a, rough = g[4] / a;
+    const float ia = 1.0f / a;
+    const float alb[3] = {g[0] * ia, g[1] * ia, g[2] * ia};
+    const float metal = g[3] * ia, rough = g[4] * ia;
     const float nb[3] = {g[5], g[6], g[7]};
     const float nn = sqrtf((nb[0] * nb[0] + nb[1] * nb[1]) + nb[2] * nb[2]);
     const bool degen = nn < 1e-12f;
