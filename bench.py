@@ -394,9 +394,26 @@ def main():
     texel_b = 16 if args.texel_format == "rgba32f" else 8
     # compulsory HBM bytes of one K5 launch: G-buffer
     # + pixel state out, entry list + per-splat records in, and the atlas
-    # charts of every splat (both families) read once.
+    # charts (both families) of every splat that composites, read once.
+    # The touched-splat count comes from one extra, untimed diagnostic frame.
     entries = r.entries_needed()
-    alg_bytes = 68 * W * H + 4 * entries + 128 * P + 2 * P * T * T * texel_b
+    touched = torch.zeros(P, dtype=torch.uint8, device=dev)
+    cam_d = _lib.camera_struct(my_views[0])
+    pst_d = px.struct(touched)
+    _lib.check(L.tsb_render_binning(C.byref(sc), C.byref(cam_d), C.byref(at), mode, args.tile,
+                                    _lib.ptr(ws.buf), ws.nbytes, ws.capacity,
+                                    _lib.ptr(ws.needed), sh), "binning")
+    _lib.check(L.tsb_render_composite(C.byref(sc), C.byref(cam_d), C.byref(at), mode, args.tile,
+                                      _lib.ptr(ws.buf), ws.nbytes, ws.capacity, _lib.ptr(gb),
+                                      C.byref(pst_d), sh), "composite")
+    n_touched = int(touched.sum(dtype=torch.int64).item())
+    entries = r.entries_needed()
+    alg_bytes = 68 * W * H + 4 * entries + 128 * P + 2 * n_touched * T * T * texel_b
+    traffic = None
+    tj = ROOT / "profiles" / "traffic.json"
+    if tj.exists():
+        tv = _json.loads(tj.read_text()).get(f"{args.config}/{args.sampler}/{args.texel_format}")
+        traffic = tv
     hbm_achieved = alg_bytes / rast_avg_s / 1e9
     fetch_rate = 2 * fragments / rast_avg_s / 1e9 if args.sampler != "flat" else 0.0
 
@@ -421,8 +438,11 @@ def main():
         "capacity_overflow": bool(overflow),
         "roofline": {"bound": "hbm", "kernel": "k_raster_fwd", "achieved": round(hbm_achieved, 2),
                      "peak": hbm_peak, "unit": "GB/s", "frac": round(hbm_achieved / hbm_peak, 4),
-                     "traffic": None, "peak_source": hbm_src,
-                     "algorithmic_bytes_per_launch": alg_bytes},
+                     "traffic": traffic, "peak_source": hbm_src,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "splats_composited": n_touched,
+                     "traffic_source": "profiles/traffic.json (ncu --set full dram__bytes_read.sum"
+                                       " + dram__bytes_write.sum of one k_raster_fwd launch)"},
         "roofline_tex": {"bound": "tex", "kernel": "k_raster_fwd",
                          "achieved": round(fetch_rate, 3), "unit": "Gfetch/s",
                          "peak": round(tex_peak, 3) if tex_peak else None,

@@ -100,6 +100,9 @@ typedef struct tsb_pixel_state {
   int32_t* last_entry;  /* sorted-entry index of the last contributor, -1 if none */
   float* final_T;       /* transmittance after the last contributor */
   float* T_last;        /* transmittance in front of the last contributor */
+  uint8_t* splat_touched; /* optional (may be NULL), P bytes: set to 1 for every
+                             splat with at least one composited fragment
+                             (diagnostics: compulsory atlas bytes of a frame) */
 } tsb_pixel_state;
 
 /* Bytes of frame workspace for P splats at W x H with `max_entries`

@@ -59,7 +59,7 @@ class Environment_t(C.Structure):
 
 class PixelState_t(C.Structure):
     _fields_ = [("n_contrib", C.c_void_p), ("last_entry", C.c_void_p),
-                ("final_T", C.c_void_p), ("T_last", C.c_void_p)]
+                ("final_T", C.c_void_p), ("T_last", C.c_void_p), ("splat_touched", C.c_void_p)]
 
 
 class SceneGrads_t(C.Structure):

@@ -328,6 +328,7 @@ struct RasterParams {
   int32_t* last_entry;
   float* final_T;
   float* T_last;
+  uint8_t* touched;
 };
 
 // A fragment's texel data in flight: the two atlas families (HW / verify)
@@ -650,6 +651,7 @@ k_raster_fwd(RasterParams p) {
             T = tsb_composite(acc, xa, a, T);
             ++n;
             last = base + k;
+            if (p.touched) p.touched[ws.geom[k].id] = 1;
             ++r_cur;
             if (!(T > teps)) { done = true; break; }
           }
@@ -940,6 +942,7 @@ int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera, const
   rp.tex_b = atlas->tex ? reinterpret_cast<AtlasTex*>(atlas->tex)->tex_b : 0;
   rp.gbuf = gbuf; rp.n_contrib = px->n_contrib; rp.last_entry = px->last_entry;
   rp.final_T = px->final_T; rp.T_last = px->T_last;
+  rp.touched = px->splat_touched;
   cudaError_t e;
   if (tile == 8) e = launch_raster<8>(mode, L.num_tiles, st, rp);
   else if (tile == 16) e = launch_raster<16>(mode, L.num_tiles, st, rp);

@@ -60,12 +60,13 @@ class PixelState:
                           torch.empty((H, W), dtype=torch.float32, device=device),
                           torch.empty((H, W), dtype=torch.float32, device=device))
 
-    def struct(self) -> _lib.PixelState_t:
+    def struct(self, touched: torch.Tensor = None) -> _lib.PixelState_t:
         s = _lib.PixelState_t()
         s.n_contrib = _lib.ptr(self.n_contrib)
         s.last_entry = _lib.ptr(self.last_entry)
         s.final_T = _lib.ptr(self.final_T)
         s.T_last = _lib.ptr(self.T_last)
+        s.splat_touched = _lib.ptr(touched)
         return s
 
 
