@@ -815,19 +815,19 @@ static int validate_frame(const tsb_scene* scene, const tsb_camera* camera, cons
     set_error("SH degree must be in [0, 3]");
     return TSB_ERR_VALUE;
   }
-  if (mode == TSB_MODE_HW && !atlas->tex) {
+  if (scene->num_splats > 0 && mode == TSB_MODE_HW && !atlas->tex) {
     set_error("HW texture mode needs an atlas texture (tsb_atlas_tex_create)");
     return TSB_ERR_VALUE;
   }
-  if (mode == TSB_MODE_VERIFY && (!atlas->family_a || !atlas->family_b)) {
+  if (scene->num_splats > 0 && mode == TSB_MODE_VERIFY && (!atlas->family_a || !atlas->family_b)) {
     set_error("verify mode needs linear atlas pages");
     return TSB_ERR_VALUE;
   }
-  if (mode == TSB_MODE_FLAT && !atlas->flat_attrs) {
+  if (scene->num_splats > 0 && mode == TSB_MODE_FLAT && !atlas->flat_attrs) {
     set_error("flat mode needs flat_attrs");
     return TSB_ERR_VALUE;
   }
-  if (mode != TSB_MODE_FLAT && !atlas->entries) {
+  if (scene->num_splats > 0 && mode != TSB_MODE_FLAT && !atlas->entries) {
     set_error("textured modes need atlas indirection entries");
     return TSB_ERR_VALUE;
   }

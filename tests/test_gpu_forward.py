@@ -246,3 +246,61 @@ def test_cfg2_full_frame_bit_exact_vs_oracle(lut_table):
     c_or, _, _ = oracle.shade(ref["gbuf"], cam, scene.environment, lut_table, scene.background)
     srh = shade_gbuffer(hw, cam, scene.environment, gio.lut(), background=scene.background)
     assert psnr(_np(srh.color), c_or) >= 50.0
+
+
+def test_empty_scene_and_odd_sizes():
+    """P = 0, and image sizes that are not tile multiples (rasterize.py
+    clips the last tiles to the image)."""
+    s = _facing_scene([0.0], [0.9], [(0.5, 0.5, 0.5)])
+    empty = Scene(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 2)),
+                  np.zeros(0), np.zeros((0, 1, 3)), 0, np.zeros((0, 2, 2, 7), np.float32),
+                  TextureConfig(2))
+    cam = Camera.look_at((0.0, 0.0, -2.0), (0.0, 0.0, 1.0), width=37, height=23)
+    gb = render_forward(empty, cam, "flat")
+    assert gb.fragment_count == 0 and float(gb.planar.abs().max()) == 0.0
+    for tile in (8, 16, 32):
+        gb = render_forward(s, cam, "perprim", tile=tile)
+        ref = oracle.render(s, cam, tile=tile)
+        assert np.array_equal(_np(gb.planar), ref["gbuf"])
+
+
+def test_splat_crossing_near_plane_gets_fullscreen_rect():
+    """Centre in front, a rect corner behind the near plane: full-screen rect
+    (rasterize.py:151-168); results still match the oracle bit for bit."""
+    s = _facing_scene([0.0], [0.9], [(0.5, 0.5, 0.5)])
+    s.tangent_v[0] = [0.0, 0.0, 1.0]          # splat plane contains the view axis
+    s.tangent_u[0] = [1.0, 0.0, 0.0]
+    s.scales[0] = [0.8, 1.0]
+    cam = Camera.look_at((0.0, 0.3, -1.0), (0.0, 0.0, 1.0), width=40, height=40, near=0.05)
+    gb, tape = render_forward(s, cam, "perprim", with_tape=True)
+    ref = oracle.render(s, cam)
+    _assert_structure_equal(tape, ref)
+    assert np.array_equal(_np(gb.planar), ref["gbuf"])
+    assert ref["rects"][0].tolist() == [0, 40, 0, 40]
+
+
+def test_bad_inputs_raise_reference_exceptions():
+    from paper_2506_13348_b200 import prepare as prep
+    s = synth.make_plane_scene(2, 2, 4, 5)
+    cam = synth.camera_ring(1, width=16, height=16)[0]
+    with pytest.raises(ValueError):
+        prep(s, cam, "atlas", None)                      # rasterize.py:220-221
+    with pytest.raises(ValueError):
+        prep(s, cam, "atlas", pack_atlases(synth.make_plane_scene(2, 2, 2, 5)))  # :223-224
+    with pytest.raises(ValueError):
+        render_forward(s, cam, "perprim", tile=12)
+    a = pack_atlases(s)
+    a.indirection.entries[0, 0] = 10_000                 # chart out of range
+    with pytest.raises(ValueError):
+        render_forward(s, cam, "atlas", a)
+
+
+def test_hw_rgba16f_and_multipage_hw_match_counts():
+    scene = synth.make_plane_scene(6, 6, 4, 3)
+    cam = synth.camera_ring(1, width=64, height=64)[0]
+    ref = oracle.render(scene, cam)
+    for fmt in ("rgba32f", "rgba16f"):
+        gb = render_forward(scene, cam, "atlas", pack_atlases(scene, max_dim=16),
+                            texel_format=fmt)                 # 3 pages, layered texture
+        assert np.array_equal(_np(gb.pixels.n_contrib), ref["n_contrib"])
+        assert psnr(_np(gb.planar)[:12], ref["gbuf"][:12]) >= 50.0
