@@ -68,7 +68,11 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   cub::DeviceRadixSort::SortPairs(nullptr, b_tile, (const uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (const int32_t*)nullptr,
                                   (int32_t*)nullptr, (int)C, 0, bits);
-  L->cub_bytes = std::max(b_depth, std::max(b_scan, b_tile));
+  size_t b_order = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b_order, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, L->num_tiles, 0, 16);
+  L->cub_bytes = std::max(std::max(b_depth, b_order), std::max(b_scan, b_tile));
 
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
@@ -91,6 +95,10 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   L->evals_in = take(C * 4);
   L->evals_out = take(C * 4);
   L->ranges = take((size_t)L->num_tiles * 8);
+  L->tcost_in = take((size_t)L->num_tiles * 4);
+  L->tcost_out = take((size_t)L->num_tiles * 4);
+  L->torder_in = take((size_t)L->num_tiles * 4);
+  L->torder_out = take((size_t)L->num_tiles * 4);
   L->counters = take(64);
   L->cub_tmp = take(L->cub_bytes);
   L->total = o;
@@ -329,6 +337,9 @@ struct RasterParams {
   float* final_T;
   float* T_last;
   uint8_t* touched;
+  int32_t num_tiles;
+  int32_t* work_counter;      // zeroed per frame
+  const int32_t* tile_order;  // tiles by descending list length (may be null)
 };
 
 // A fragment's texel data in flight: the two atlas families (HW / verify)
@@ -522,11 +533,22 @@ k_raster_fwd(RasterParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem& ws = *reinterpret_cast<WarpSmem*>(s_raw + (size_t)warp * kRasterWarpSmem);
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const int tile = blockIdx.x;
-  const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
   const float teps = (float)TSB_TRANSMIT_EPS;
+  (void)WARPS;
 
-  for (int blk = warp; blk < NBLK; blk += WARPS) {
+  // Persistent warps: each warp pulls (tile, 8x4 block) work units from a
+  // global counter, in descending order of the tile's list length (heavy
+  // silhouette tiles first), so the frame has no long tail.
+  const int num_units = p.num_tiles * NBLK;
+  while (true) {
+    int unit = 0;
+    if (lane == 0) unit = atomicAdd(p.work_counter, 1);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= num_units) break;
+    const int tile = p.tile_order ? p.tile_order[unit / NBLK] : unit / NBLK;
+    const int blk = unit % NBLK;
+    const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
+    {
     const int bx0 = (tile % p.tiles_x) * TILE + (blk % WX) * 8;
     const int by0 = (tile / p.tiles_x) * TILE + (blk / WX) * 4;
     if (bx0 >= p.W || by0 >= p.H) continue;
@@ -669,7 +691,19 @@ k_raster_fwd(RasterParams p) {
       p.final_T[pix] = T;
       p.T_last[pix] = T_last;
     }
+    }
   }
+}
+
+// Sort key for the persistent rasterizer's schedule: tiles by descending
+// list length (longest-processing-time first).
+__global__ void k_tile_cost(int32_t n, const int32_t* __restrict__ ranges,
+                            uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int c = ranges[2 * t + 1] - ranges[2 * t];
+  keys[t] = 0xFFFFu - (uint32_t)(c < 0xFFFF ? c : 0xFFFF);
+  vals[t] = t;
 }
 
 // ---------------------------------------------------------------------------
@@ -758,14 +792,22 @@ template <int TILE, int MODE>
 inline cudaError_t launch_raster_mode(int blocks, cudaStream_t st, const RasterParams& rp) {
   constexpr int threads = TILE * TILE < 256 ? TILE * TILE : 256;
   const size_t smem = (size_t)(threads / 32) * kRasterWarpSmem;
-  static bool configured = false;  // per instantiation; attribute is per function
-  if (!configured) {
+  static int resident = 0;  // per instantiation: persistent grid size
+  if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(k_raster_fwd<TILE, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+      return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_fwd<TILE, MODE>,
+                                                           threads, smem)) != cudaSuccess)
+      return e;
+    resident = std::max(1, sms * per_sm);
   }
-  k_raster_fwd<TILE, MODE><<<blocks, threads, smem, st>>>(rp);
+  const int grid = std::min(blocks, resident);
+  k_raster_fwd<TILE, MODE><<<grid, threads, smem, st>>>(rp);
   return cudaGetLastError();
 }
 
@@ -943,6 +985,24 @@ int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera, const
   rp.gbuf = gbuf; rp.n_contrib = px->n_contrib; rp.last_entry = px->last_entry;
   rp.final_T = px->final_T; rp.T_last = px->T_last;
   rp.touched = px->splat_touched;
+  rp.num_tiles = L.num_tiles;
+  rp.work_counter = reinterpret_cast<int32_t*>(ws_ptr<int64_t>(ws, L.counters) + 1);
+  TSB_CUDA(cudaMemsetAsync(rp.work_counter, 0, 4, st));
+  rp.tile_order = nullptr;
+#ifndef TSB_NO_TILE_ORDER
+  {
+    uint32_t* kin = ws_ptr<uint32_t>(ws, L.tcost_in);
+    int32_t* vin = ws_ptr<int32_t>(ws, L.torder_in);
+    k_tile_cost<<<(L.num_tiles + 255) / 256, 256, 0, st>>>(L.num_tiles, rp.ranges, kin, vin);
+    TSB_CHECK_LAUNCH("k_tile_cost");
+    size_t cb = L.cub_bytes;
+    TSB_CUDA(cub::DeviceRadixSort::SortPairs(ws_ptr<char>(ws, L.cub_tmp), cb, kin,
+                                             ws_ptr<uint32_t>(ws, L.tcost_out), vin,
+                                             ws_ptr<int32_t>(ws, L.torder_out), L.num_tiles, 0,
+                                             16, st));
+    rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);
+  }
+#endif
   cudaError_t e;
   if (tile == 8) e = launch_raster<8>(mode, L.num_tiles, st, rp);
   else if (tile == 16) e = launch_raster<16>(mode, L.num_tiles, st, rp);
