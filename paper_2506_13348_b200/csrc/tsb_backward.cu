@@ -27,6 +27,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "tsb_internal.cuh"
 
 namespace tsb {
@@ -329,6 +331,9 @@ struct RasterBwdParams {
   const float* dgbuf;
   float* acc;          // P x kAccWords
   float* dtexels;      // P x T x T x 7
+  int32_t num_tiles;
+  int32_t* work_counter;
+  const int32_t* tile_order;
 };
 
 struct BwdWarpSmem {
@@ -365,13 +370,19 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
   const int TILE = p.tile;
   const int wx = TILE / 8;
   const int nblk = TILE * TILE / 32;
-  const int tile = blockIdx.x;
-  const int start = p.ranges[2 * tile];
   const int T = p.T;
-  const float teps = (float)TSB_TRANSMIT_EPS;
-  (void)teps;
-
-  for (int blk = warp; blk < nblk; blk += 8) {
+  // persistent warps over (tile, 8x4 block) units, heaviest tiles first
+  // (the forward's schedule order, left in the workspace)
+  const int num_units = p.num_tiles * nblk;
+  while (true) {
+    int unit = 0;
+    if (lane == 0) unit = atomicAdd(p.work_counter, 1);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= num_units) break;
+    const int tile = p.tile_order ? p.tile_order[unit / nblk] : unit / nblk;
+    const int blk = unit % nblk;
+    const int start = p.ranges[2 * tile];
+    {
     const int bx0 = (tile % p.tiles_x) * TILE + (blk % wx) * 8;
     const int by0 = (tile / p.tiles_x) * TILE + (blk / wx) * 4;
     if (bx0 >= p.W || by0 >= p.H) continue;
@@ -581,6 +592,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
         }
       }
     }
+  }
   }
 }
 
@@ -865,7 +877,19 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera, const 
   rp.dgbuf = dgbuf;
   rp.acc = acc;
   rp.dtexels = grads->texels;
-  k_raster_bwd<<<L.num_tiles, 256, 0, st>>>(rp);
+  rp.num_tiles = L.num_tiles;
+  rp.work_counter = reinterpret_cast<int32_t*>(const_cast<int64_t*>(ws_ptr<int64_t>(ws, L.counters)) + 2);
+  rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);
+  TSB_CUDA(cudaMemsetAsync(rp.work_counter, 0, 4, st));
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 0, per_sm = 0;
+    TSB_CUDA(cudaGetDevice(&dev));
+    TSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_bwd, 256, 0));
+    resident = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  k_raster_bwd<<<std::min(L.num_tiles, resident), 256, 0, st>>>(rp);
   TSB_CHECK_LAUNCH("k_raster_bwd");
   FinishParams fp;
   fp.cam = to_cam(camera);
