@@ -66,17 +66,55 @@ class Renderer:
     def entries_needed(self) -> int:
         return int(self.prep.workspace.needed.item())
 
-    def render(self, camera, *, check: bool = True, want_split: bool = False, stream=None):
+    def render(self, camera, *, check: bool = True, want_split: bool = False, stream=None,
+               color=None):
         """Forward + shade one view. Returns (color (H,W,3), GBuffer), both on
-        the GPU; buffers are reused across calls of the same size."""
+        the GPU; buffers are reused across calls of the same size (pass
+        `color` to shade into a caller-owned buffer instead)."""
         W, H = int(camera.width), int(camera.height)
         gb, px, col, dif, spe = self._buffers(W, H)
+        if color is not None:
+            col = color
         gbuf, _ = render_prepared(self.prep, camera, self.tile, out=gb, pixels=px, check=check,
                                   stream=stream)
         shade_planar(gb, camera, self.env, self.background, color=col,
                      diffuse=dif if want_split else None, specular=spe if want_split else None,
                      want_split=want_split, stream=stream)
         return col, gbuf
+
+    def stream_views(self, cameras, host_out=None):
+        """Render a sequence of views and read each colour image back to
+        pinned host memory, overlapping frame i's device->host copy with
+        frame i+1's render (double-buffered outputs, a dedicated copy stream).
+        Yields (index, host colour tensor) as each copy completes; the host
+        buffer is reused two frames later."""
+        cams = list(cameras)
+        if not cams:
+            return
+        W, H = int(cams[0].width), int(cams[0].height)
+        dev = self.device
+        dcol = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)]
+        hcol = host_out or [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True)
+                            for _ in range(2)]
+        compute = torch.cuda.current_stream(dev)
+        copy = torch.cuda.Stream(dev)
+        done = [torch.cuda.Event(), torch.cuda.Event()]
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        for i, cam in enumerate(cams):
+            b = i & 1
+            if i >= 2:
+                done[b].synchronize()           # host buffer b free again
+                yield i - 2, hcol[b]
+            compute.wait_event(done[b]) if i >= 2 else None  # device buffer b free
+            self.render(cam, check=False, stream=compute, color=dcol[b])
+            ready[b].record(compute)
+            copy.wait_event(ready[b])
+            with torch.cuda.stream(copy):
+                hcol[b].copy_(dcol[b], non_blocking=True)
+            done[b].record(copy)
+        for j in range(max(0, len(cams) - 2), len(cams)):
+            done[j & 1].synchronize()
+            yield j, hcol[j & 1]
 
     def shade(self, gbuf: GBuffer, camera) -> ShadeResult:
         c, d, s = shade_planar(gbuf.planar, camera, self.env, self.background)
