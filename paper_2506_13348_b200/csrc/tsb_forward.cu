@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
 
   GeomRec g;
   tsb_make_lin(r.m, op, g.lin);
-  g.r2lo = tsb_lin_r2lo(g.lin);
+  g.r2lo = tsb_lin_r2lo(g.lin[11]);
   p.rects[id] = make_uint2((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
                            (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
   int32_t tb[4];
@@ -413,12 +413,30 @@ __device__ __forceinline__ float frag_composite(const MatRec& m, const Frag& f, 
 constexpr int kRasterCap = TSB_RASTER_CAP;  // texturing window (pairs), CAP/32 per lane
 
 // Warp-private shared memory of the rasterizer.
+// What the decide loop reads of one staged splat: 48 bytes, three
+// broadcast 128-bit loads (a 48-byte lane stride also makes the staging
+// stores conflict-free).
+struct __align__(16) DecRec {
+  float lin[10];      // L0..L9: D, Nu, Nv forms and det
+  float r2hi;         // L11
+  uint32_t pixmask;   // pixels of the current 8x4 block inside the test box
+};
+
 struct WarpSmem {
-  GeomRec geom[32];           // staged step: intersection forms + test box
-  MatRec mat[32];             // staged step: frame, SH radiance, chart
+  // staged step, AoS for the decide loop (all lanes read the same splat)
+  DecRec dec[32];
+  int32_t sid[32];            // splat ids
+  // the same step as structure-of-arrays for texturing / blending, where
+  // every lane reads a different splat: conflict-free 32-bit loads
+  float lin[11][32];          // intersection forms L0..L10
+  float frame[9][32];         // t_u, t_v, t_u x t_v
+  float texo[2][32];          // chart origin (texels)
+  int32_t page[32];
+  int32_t loff[32];
+  float lind[3][32];          // clamped SH radiance
   uint32_t act[32];           // lanes with > r live pairs, per round r
   int32_t rbase[32];          // first pair index of round r
-  float2 xy[32];              // camera-plane coordinates of the 32 pixels
+  float px_x[32], px_y[32];   // camera-plane coordinates of the 32 pixels
   float res[10][kRasterCap];  // textured pair attributes (+ z, alpha)
   uint16_t pairs[32 * 32];    // (lane << 5) | k, round-robin order
 };
@@ -436,16 +454,16 @@ struct PairFetch {
 // mode); no use of the fetched data yet, so several pairs overlap.
 template <int MODE>
 __device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem& ws, int q,
-                                           PairFetch& f) {
+                                           float2 xy, PairFetch& f) {
   const int k = q & 31;
-  const float2 xy = ws.xy[q >> 5];
-  const GeomRec& g = ws.geom[k];
-  const MatRec& m = ws.mat[k];
+  float L[11];
+#pragma unroll
+  for (int c = 0; c < 11; ++c) L[c] = ws.lin[c][k];
   float u, v;
-  tsb_eval_lin(g.lin, xy.x, xy.y, p.near_f, &u, &v, &f.z, &f.a);
+  tsb_uvza_lin(L, xy.x, xy.y, &u, &v, &f.z, &f.a);
   f.k = k;
   if (MODE == TSB_MODE_FLAT) {
-    const float* fl = p.flat + 5 * g.id;
+    const float* fl = p.flat + 5 * ws.sid[k];
     f.A = make_float4(__ldg(fl), __ldg(fl + 1), __ldg(fl + 2), __ldg(fl + 4));
     f.B = make_float4(0.f, 0.f, __ldg(fl + 3), 0.f);
     return;
@@ -453,18 +471,20 @@ __device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem
   tsb_texc tc;
   tsb_texel_coords(u, v, p.T, &tc);
   if (MODE == TSB_MODE_HW) {
-    const float sx = m.tex_x + tc.xs + 0.5f;
-    const float sy = m.tex_y + tc.yt + 0.5f;
+    const float sx = ws.texo[0][k] + tc.xs + 0.5f;
+    const float sy = ws.texo[1][k] + tc.yt + 0.5f;
+    const int page = ws.page[k];
 #ifdef TSB_PROBE_NOTEX
     f.A = make_float4(sx * 1e-9f, 0.5f, 0.5f, 0.5f);
     f.B = make_float4(0.5f, sy * 1e-9f + 0.5f, 0.2f, 0.f);
 #else
-    f.A = tex2DLayered<float4>(p.tex_a, sx, sy, m.page);
-    f.B = tex2DLayered<float4>(p.tex_b, sx, sy, m.page);
+    f.A = tex2DLayered<float4>(p.tex_a, sx, sy, page);
+    f.B = tex2DLayered<float4>(p.tex_b, sx, sy, page);
 #endif
   } else {
     const int S = p.tstride;
-    const int r0 = m.lin_off + tc.j0 * p.page_w, r1 = m.lin_off + tc.j1 * p.page_w;
+    const int loff = ws.loff[k];
+    const int r0 = loff + tc.j0 * p.page_w, r1 = loff + tc.j1 * p.page_w;
     const float4 a00 = __ldg(p.fam_a + S * (r0 + tc.i0)), a01 = __ldg(p.fam_a + S * (r0 + tc.i1));
     const float4 a10 = __ldg(p.fam_a + S * (r1 + tc.i0)), a11 = __ldg(p.fam_a + S * (r1 + tc.i1));
     const float4 b00 = __ldg(p.fam_b + S * (r0 + tc.i0)), b01 = __ldg(p.fam_b + S * (r0 + tc.i1));
@@ -483,24 +503,34 @@ __device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem
 // Stage 2: normal decode (rasterize.py:313-314) and the pair's attribute
 // row into result slot t.
 template <int MODE>
-__device__ __forceinline__ void pair_finish(WarpSmem& ws, const PairFetch& f, int t) {
-  const MatRec& m = ws.mat[f.k];
+__device__ __forceinline__ void pair_result(const WarpSmem& ws, const PairFetch& f, float* rv) {
+  float fr[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) fr[c] = ws.frame[c][f.k];
   float nw[3];
   if (MODE == TSB_MODE_FLAT) {
-    nw[0] = m.frame[6]; nw[1] = m.frame[7]; nw[2] = m.frame[8];
+    nw[0] = fr[6]; nw[1] = fr[7]; nw[2] = fr[8];
   } else {
-    tsb_decode_normal(f.B.x, f.B.y, m.frame, nw);
+    tsb_decode_normal(f.B.x, f.B.y, fr, nw);
   }
-  ws.res[0][t] = f.A.x;
-  ws.res[1][t] = f.A.y;
-  ws.res[2][t] = f.A.z;
-  ws.res[3][t] = f.B.z;  // metallic
-  ws.res[4][t] = f.A.w;  // roughness
-  ws.res[5][t] = nw[0];
-  ws.res[6][t] = nw[1];
-  ws.res[7][t] = nw[2];
-  ws.res[8][t] = f.z;
-  ws.res[9][t] = f.a;
+  rv[0] = f.A.x;
+  rv[1] = f.A.y;
+  rv[2] = f.A.z;
+  rv[3] = f.B.z;  // metallic
+  rv[4] = f.A.w;  // roughness
+  rv[5] = nw[0];
+  rv[6] = nw[1];
+  rv[7] = nw[2];
+  rv[8] = f.z;
+  rv[9] = f.a;
+}
+
+template <int MODE>
+__device__ __forceinline__ void pair_finish(WarpSmem& ws, const PairFetch& f, int t) {
+  float rv[10];
+  pair_result<MODE>(ws, f, rv);
+#pragma unroll
+  for (int c = 0; c < 10; ++c) ws.res[c][t] = rv[c];
 }
 
 // K5. One CTA per TILE x TILE tile; each warp owns 8 x 4 pixel blocks of the
@@ -557,7 +587,8 @@ k_raster_fwd(RasterParams p) {
     const float x = (float)tsb_pixel_x(&p.cam, px), y = (float)tsb_pixel_y(&p.cam, py);
     const int bx1 = min(bx0 + 8, p.W), by1 = min(by0 + 4, p.H);
     __syncwarp();
-    ws.xy[lane] = make_float2(x, y);
+    ws.px_x[lane] = x;
+    ws.px_y[lane] = y;
 
     float acc[13];
 #pragma unroll
@@ -574,11 +605,38 @@ k_raster_fwd(RasterParams p) {
       __syncwarp();
       if (e < end) {
         const int id = __ldg(p.evals + e);
-        const GeomRec g = p.geom[id];
-        ws.geom[lane] = g;
-        ws.mat[lane] = p.mat[id];
-        hit = (int)(g.bx & 0xFFFF) < bx1 && (int)(g.bx >> 16) > bx0 &&
-              (int)(g.by & 0xFFFF) < by1 && (int)(g.by >> 16) > by0;
+        const float4* gq = reinterpret_cast<const float4*>(p.geom + id);
+        const float4 gv[4] = {__ldg(gq), __ldg(gq + 1), __ldg(gq + 2), __ldg(gq + 3)};
+        // test box -> mask of this block's pixels inside it
+        const uint32_t gbx = __float_as_uint(gv[3].x), gby = __float_as_uint(gv[3].y);
+        const int cx0 = min(max((int)(gbx & 0xFFFF) - bx0, 0), 8);
+        const int cx1 = min(max((int)(gbx >> 16) - bx0, 0), bx1 - bx0);
+        const int cy0 = min(max((int)(gby & 0xFFFF) - by0, 0), 4);
+        const int cy1 = min(max((int)(gby >> 16) - by0, 0), by1 - by0);
+        uint32_t pm = 0;
+        if (cx1 > cx0 && cy1 > cy0) {
+          const uint32_t row = ((1u << cx1) - 1u) & ~((1u << cx0) - 1u);
+          const uint32_t rows = (uint32_t)(((1ull << (8 * cy1)) - 1ull) & ~((1ull << (8 * cy0)) - 1ull));
+          pm = (row * 0x01010101u) & rows;
+        }
+        hit = pm != 0;
+        float4* d = reinterpret_cast<float4*>(&ws.dec[lane]);
+        d[0] = gv[0];
+        d[1] = gv[1];
+        d[2] = make_float4(gv[2].x, gv[2].y, gv[2].w, __uint_as_float(pm));
+        ws.sid[lane] = id;
+        const float gl[11] = {gv[0].x, gv[0].y, gv[0].z, gv[0].w, gv[1].x, gv[1].y,
+                              gv[1].z, gv[1].w, gv[2].x, gv[2].y, gv[2].z};
+#pragma unroll
+        for (int c = 0; c < 11; ++c) ws.lin[c][lane] = gl[c];
+        const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
+        const float4 m0 = __ldg(mq), m1 = __ldg(mq + 1), m2 = __ldg(mq + 2), m3 = __ldg(mq + 3);
+        ws.frame[0][lane] = m0.x; ws.frame[1][lane] = m0.y; ws.frame[2][lane] = m0.z;
+        ws.frame[3][lane] = m0.w; ws.frame[4][lane] = m1.x; ws.frame[5][lane] = m1.y;
+        ws.frame[6][lane] = m1.z; ws.frame[7][lane] = m1.w; ws.frame[8][lane] = m2.x;
+        ws.lind[0][lane] = m2.y; ws.lind[1][lane] = m2.z; ws.lind[2][lane] = m2.w;
+        ws.texo[0][lane] = m3.x; ws.texo[1][lane] = m3.y;
+        ws.page[lane] = __float_as_int(m3.z); ws.loff[lane] = __float_as_int(m3.w);
       }
       const uint32_t cand = __ballot_sync(0xffffffffu, hit);
       __syncwarp();
@@ -597,11 +655,9 @@ k_raster_fwd(RasterParams p) {
           }
 #pragma unroll
           for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
-            const GeomRec& g = ws.geom[kk[j]];
-            const bool in =
-                (unsigned)(px - (int)(g.bx & 0xFFFF)) < (unsigned)((int)(g.bx >> 16) - (int)(g.bx & 0xFFFF)) &&
-                (unsigned)(py - (int)(g.by & 0xFFFF)) < (unsigned)((int)(g.by >> 16) - (int)(g.by & 0xFFFF));
-            const int r = tsb_predecide_lin_nb(g.lin, g.r2lo, x, y, p.near_f);
+            const DecRec& g = ws.dec[kk[j]];
+            const bool in = (g.pixmask >> lane) & 1u;
+            const int r = tsb_predecide_lin_nb(g.lin, g.r2hi, x, y, p.near_f);
             live |= (in && r == 1 ? 1u : 0u) << kk[j];
             undecided |= (in && r == 2 ? 1u : 0u) << kk[j];
           }
@@ -609,11 +665,14 @@ k_raster_fwd(RasterParams p) {
         // the rare candidates near the alpha cut / near plane: exact path
         for (uint32_t m = undecided; m; m &= m - 1) {
           const int k = __ffs(m) - 1;
-          const GeomRec& g = ws.geom[k];
+          float L[12];
+#pragma unroll
+          for (int c = 0; c < 11; ++c) L[c] = ws.lin[c][k];
+          L[11] = ws.dec[k].r2hi;
           float u, v, z, a;
-          int r = tsb_eval_lin(g.lin, x, y, p.near_f, &u, &v, &z, &a);
+          int r = tsb_eval_lin(L, x, y, p.near_f, &u, &v, &z, &a);
           if (r == 2) {
-            const double* m64 = p.m64 + (size_t)kM64Stride * g.id;
+            const double* m64 = p.m64 + (size_t)kM64Stride * ws.sid[k];
             r = tsb_live_f64(m64, m64[9], tsb_pixel_x(&p.cam, px), tsb_pixel_y(&p.cam, py),
                              p.cam.near_z);
           }
@@ -647,7 +706,10 @@ k_raster_fwd(RasterParams p) {
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
             const int t = w + lane + 32 * j;
-            if (t < total) pair_issue<MODE>(p, ws, ws.pairs[t], f[j]);
+            if (t < total) {
+              const int q = ws.pairs[t];
+              pair_issue<MODE>(p, ws, q, make_float2(ws.px_x[q >> 5], ws.px_y[q >> 5]), f[j]);
+            }
           }
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
@@ -666,14 +728,14 @@ k_raster_fwd(RasterParams p) {
             float xa[12];
 #pragma unroll
             for (int c = 0; c < 8; ++c) xa[c] = ws.res[c][t];
-            xa[8] = ws.mat[k].l_ind[0]; xa[9] = ws.mat[k].l_ind[1]; xa[10] = ws.mat[k].l_ind[2];
+            xa[8] = ws.lind[0][k]; xa[9] = ws.lind[1][k]; xa[10] = ws.lind[2][k];
             xa[11] = ws.res[8][t];
             const float a = ws.res[9][t];
             T_last = T;
             T = tsb_composite(acc, xa, a, T);
             ++n;
             last = base + k;
-            if (p.touched) p.touched[ws.geom[k].id] = 1;
+            if (p.touched) p.touched[ws.sid[k]] = 1;
             ++r_cur;
             if (!(T > teps)) { done = true; break; }
           }
