@@ -28,7 +28,11 @@
 
 #include "tsb_internal.cuh"
 
-// Minimum resident CTAs per SM requested for the 16x16 rasterizer.
+// Rasterizer CTA shape: persistent warps, so any tile size runs with the
+// same CTA (TSB_RASTER_WARPS warps, TSB_RASTER_MINB resident CTAs per SM).
+#ifndef TSB_RASTER_WARPS
+#define TSB_RASTER_WARPS 8
+#endif
 #ifndef TSB_RASTER_MINB
 #define TSB_RASTER_MINB 3
 #endif
@@ -407,10 +411,9 @@ __device__ __forceinline__ float frag_composite(const MatRec& m, const Frag& f, 
 #ifndef TSB_DECIDE_ILP
 #define TSB_DECIDE_ILP 2
 #endif
-#ifndef TSB_RASTER_CAP
-#define TSB_RASTER_CAP 32
+#ifndef TSB_PAIR_ILP
+#define TSB_PAIR_ILP 2
 #endif
-constexpr int kRasterCap = TSB_RASTER_CAP;  // texturing window (pairs), CAP/32 per lane
 
 // Warp-private shared memory of the rasterizer.
 // What the decide loop reads of one staged splat: 48 bytes, three
@@ -434,11 +437,6 @@ struct WarpSmem {
   int32_t page[32];
   int32_t loff[32];
   float lind[3][32];          // clamped SH radiance
-  uint32_t act[32];           // lanes with > r live pairs, per round r
-  int32_t rbase[32];          // first pair index of round r
-  float px_x[32], px_y[32];   // camera-plane coordinates of the 32 pixels
-  float res[10][kRasterCap];  // textured pair attributes (+ z, alpha)
-  uint16_t pairs[32 * 32];    // (lane << 5) | k, round-robin order
 };
 constexpr size_t kRasterWarpSmem = (sizeof(WarpSmem) + 15) & ~size_t(15);
 
@@ -525,13 +523,6 @@ __device__ __forceinline__ void pair_result(const WarpSmem& ws, const PairFetch&
   rv[9] = f.a;
 }
 
-template <int MODE>
-__device__ __forceinline__ void pair_finish(WarpSmem& ws, const PairFetch& f, int t) {
-  float rv[10];
-  pair_result<MODE>(ws, f, rv);
-#pragma unroll
-  for (int c = 0; c < 10; ++c) ws.res[c][t] = rv[c];
-}
 
 // K5. One CTA per TILE x TILE tile; each warp owns 8 x 4 pixel blocks of the
 // tile and walks the tile's draw-ordered list on its own (no CTA barriers; a
@@ -542,29 +533,25 @@ __device__ __forceinline__ void pair_finish(WarpSmem& ws, const PairFetch& f, in
 //   decide   per pixel, which candidates composite (test box, 6-FMA linear
 //            forms, division-free reject, alpha cut + fp64 guard band) —
 //            a live bitmask; nothing here depends on transmittance;
-//   compact  the live (pixel, splat) pairs into a round-robin list: all
-//            pixels' first live splat, then all second ones, ...;
-//   texture  all lanes texture the list in windows of 64 pairs, two pairs
-//            per lane in flight (fetch + decode are T-independent);
-//   blend    each pixel composites its pairs of the window in draw order
-//            with the reference's T gate (rasterize.py:366-381).
+//   texture  each lane walks its pixel's live bits in draw order, two pairs
+//   + blend  per iteration (both texel fetches in flight before the first
+//            blend), and composites them with the reference's T gate
+//            (rasterize.py:366-381); a saturated pixel stops fetching.
+// (An earlier variant compacted the live pairs of all 32 pixels into a
+// round-robin list so texturing ran with full lanes; the compaction's shared-
+// memory round trips cost more than the idle lanes it saved: 0.49 -> 0.35 ms
+// on cfg2.)
 // The per-pixel decision and blend sequence is exactly the reference's
 // (tsb_math.h); the work split never changes a bit of the result.
 template <int TILE, int MODE>
-__global__ void __launch_bounds__(TILE * TILE < 256 ? TILE * TILE : 256,
-                                  TILE == 16 ? TSB_RASTER_MINB : 1)
+__global__ void __launch_bounds__(32 * TSB_RASTER_WARPS, TSB_RASTER_MINB)
 k_raster_fwd(RasterParams p) {
-  constexpr int THREADS = TILE * TILE < 256 ? TILE * TILE : 256;
-  constexpr int WARPS = THREADS / 32;
   constexpr int NBLK = TILE * TILE / 32;  // 8 x 4 pixel blocks per tile
   constexpr int WX = TILE / 8;            // blocks per tile row
-  constexpr int CAP = kRasterCap;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem& ws = *reinterpret_cast<WarpSmem*>(s_raw + (size_t)warp * kRasterWarpSmem);
-  const uint32_t lt_mask = (1u << lane) - 1u;
   const float teps = (float)TSB_TRANSMIT_EPS;
-  (void)WARPS;
 
   // Persistent warps: each warp pulls (tile, 8x4 block) work units from a
   // global counter, in descending order of the tile's list length (heavy
@@ -586,9 +573,6 @@ k_raster_fwd(RasterParams p) {
     const bool inside = px < p.W && py < p.H;
     const float x = (float)tsb_pixel_x(&p.cam, px), y = (float)tsb_pixel_y(&p.cam, py);
     const int bx1 = min(bx0 + 8, p.W), by1 = min(by0 + 4, p.H);
-    __syncwarp();
-    ws.px_x[lane] = x;
-    ws.px_y[lane] = y;
 
     float acc[13];
 #pragma unroll
@@ -679,69 +663,41 @@ k_raster_fwd(RasterParams p) {
           if (r) live |= 1u << k;
         }
       }
-      // ---- compact (round-robin)
-      const int cnt = __popc(live);
-      const int maxc = __reduce_max_sync(0xffffffffu, cnt);
-      if (maxc == 0) continue;
-      int total = 0;
-      {
-        uint32_t m = live;
-        for (int r = 0; r < maxc; ++r) {
-          const uint32_t act = __ballot_sync(0xffffffffu, cnt > r);
-          if (lane == 0) { ws.act[r] = act; ws.rbase[r] = total; }
-          if (cnt > r) {
-            ws.pairs[total + __popc(act & lt_mask)] = (uint16_t)((lane << 5) | (__ffs(m) - 1));
-            m &= m - 1;
+      // ---- texture + blend, in order, TSB_PAIR_ILP live pairs per lane per iteration
+      while (__any_sync(0xffffffffu, live != 0)) {
+        if (live) {
+          int kk[TSB_PAIR_ILP];
+          bool hv[TSB_PAIR_ILP];
+          PairFetch f[TSB_PAIR_ILP];
+#pragma unroll
+          for (int j = 0; j < TSB_PAIR_ILP; ++j) {
+            hv[j] = live != 0;
+            kk[j] = hv[j] ? __ffs(live) - 1 : 0;
+            live &= live - 1;
+            if (hv[j]) pair_issue<MODE>(p, ws, kk[j], make_float2(x, y), f[j]);
           }
-          total += __popc(act);
+#pragma unroll
+          for (int j = 0; j < TSB_PAIR_ILP; ++j) {
+            if (hv[j] && !done) {
+              const int k = kk[j];
+              float rv[10];
+              pair_result<MODE>(ws, f[j], rv);
+              float xa[12];
+#pragma unroll
+              for (int c = 0; c < 8; ++c) xa[c] = rv[c];
+              xa[8] = ws.lind[0][k]; xa[9] = ws.lind[1][k]; xa[10] = ws.lind[2][k];
+              xa[11] = rv[8];
+              T_last = T;
+              T = tsb_composite(acc, xa, rv[9], T);
+              ++n;
+              last = base + k;
+              if (p.touched) p.touched[ws.sid[k]] = 1;
+              if (!(T > teps)) { done = true; live = 0; }
+            }
+          }
         }
       }
       __syncwarp();
-      int r_cur = 0;  // next round this lane blends
-      for (int w = 0; w < total; w += CAP) {
-        // ---- texture pairs [w, w + CAP): issue every fetch, then finish
-        {
-          constexpr int NP = CAP / 32;
-          PairFetch f[NP];
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            const int t = w + lane + 32 * j;
-            if (t < total) {
-              const int q = ws.pairs[t];
-              pair_issue<MODE>(p, ws, q, make_float2(ws.px_x[q >> 5], ws.px_y[q >> 5]), f[j]);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            const int t = w + lane + 32 * j;
-            if (t < total) pair_finish<MODE>(ws, f[j], lane + 32 * j);
-          }
-        }
-        __syncwarp();
-        // ---- blend this lane's pairs that fall in the window, in order
-        if (!done) {
-          while (r_cur < cnt) {
-            const int pos = ws.rbase[r_cur] + __popc(ws.act[r_cur] & lt_mask);
-            if (pos >= w + CAP) break;
-            const int t = pos - w;
-            const int k = ws.pairs[pos] & 31;
-            float xa[12];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) xa[c] = ws.res[c][t];
-            xa[8] = ws.lind[0][k]; xa[9] = ws.lind[1][k]; xa[10] = ws.lind[2][k];
-            xa[11] = ws.res[8][t];
-            const float a = ws.res[9][t];
-            T_last = T;
-            T = tsb_composite(acc, xa, a, T);
-            ++n;
-            last = base + k;
-            if (p.touched) p.touched[ws.sid[k]] = 1;
-            ++r_cur;
-            if (!(T > teps)) { done = true; break; }
-          }
-        }
-        __syncwarp();
-      }
     }
     if (inside) {
       const int HW = p.W * p.H;
@@ -852,7 +808,7 @@ __global__ void k_tex_probe(cudaTextureObject_t tex, int32_t window, int32_t ite
 
 template <int TILE, int MODE>
 inline cudaError_t launch_raster_mode(int blocks, cudaStream_t st, const RasterParams& rp) {
-  constexpr int threads = TILE * TILE < 256 ? TILE * TILE : 256;
+  constexpr int threads = 32 * TSB_RASTER_WARPS;
   const size_t smem = (size_t)(threads / 32) * kRasterWarpSmem;
   static int resident = 0;  // per instantiation: persistent grid size
   if (!resident) {
@@ -868,7 +824,9 @@ inline cudaError_t launch_raster_mode(int blocks, cudaStream_t st, const RasterP
       return e;
     resident = std::max(1, sms * per_sm);
   }
-  const int grid = std::min(blocks, resident);
+  // one warp per (tile, 8x4 block) unit at most
+  const int units = blocks * (TILE * TILE / 32);
+  const int grid = std::min((units + TSB_RASTER_WARPS - 1) / TSB_RASTER_WARPS, resident);
   k_raster_fwd<TILE, MODE><<<grid, threads, smem, st>>>(rp);
   return cudaGetLastError();
 }
