@@ -2,8 +2,9 @@
 //
 //   K1 k_preprocess     per splat, fp64: rect/cull, centre depth key, M, frame,
 //                       SH radiance -> GeomRec / MatRec / fp64 M
-//   S1 depth sort       stable LSD radix sort of fp64 depth bits (ids in id
-//                       order => ties broken by id, == np.lexsort((ids, z)))
+//   S1 depth sort       stable LSD radix sort of a 24-bit depth key (ids in
+//                       id order) + k_fix_runs: exact (fp64 z, id) order,
+//                       == np.lexsort((ids, z))
 //   K2 k_rank_counts    per rank: tile count, rank of id
 //   S2 exclusive scan   entry offsets in draw order
 //   K3 k_duplicate_lb   (tile, id) entries in draw order, binned by the test
@@ -50,6 +51,11 @@ int cuda_fail(const char* what, cudaError_t err) {
 
 static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
+// Depth sort key width: 24 bits of (bits(z) - bits(near)) >> 32 (three
+// 8-bit radix passes); equal keys are re-ordered exactly by k_fix_runs.
+constexpr int kDepthKeyBits = 24;
+constexpr uint32_t kDepthCulled = (1u << kDepthKeyBits) - 1u;
+
 bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLayout* L) {
   if (P < 0 || W <= 0 || H <= 0 || cap < 0) return false;
   if (tile != 8 && tile != 16 && tile != 32) return false;
@@ -66,7 +72,7 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   size_t b_depth = 0, b_scan = 0, b_tile = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, b_depth, (const uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (const int32_t*)nullptr,
-                                  (int32_t*)nullptr, (int)Pn, 0, 32);
+                                  (int32_t*)nullptr, (int)Pn, 0, kDepthKeyBits);
   cub::DeviceScan::ExclusiveSum(nullptr, b_scan, (const int32_t*)nullptr,
                                 (int32_t*)nullptr, (int)Pn);
   cub::DeviceRadixSort::SortPairs(nullptr, b_tile, (const uint32_t*)nullptr,
@@ -182,18 +188,19 @@ __global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
   for (int k = 0; k < 9; ++k) m64[k] = r.m[k];
   m64[9] = op;
 
-  // 32-bit sort key: (bits(z) - bits(near)) >> 24 is monotone in z for
-  // z > near (positive doubles order like their bit patterns); equal keys
-  // (depths within ~4e-9 relative) are re-ordered by k_fix_runs on the full
-  // 64-bit pattern, so the result is the exact (z, id) order.
+  // 24-bit sort key: (bits(z) - bits(near)) >> 32 is monotone in z for
+  // z > near (positive doubles order like their bit patterns; 2^-20
+  // relative resolution over 16 binades, farther depths clamp); equal keys
+  // are re-ordered by k_fix_runs on the full 64-bit pattern, so the result
+  // is the exact (z, id) order.
   const uint64_t full = tsb_f64_bits(r.view_z);
   p.dkeys[id] = r.keep ? full : ~0ull;
-  uint64_t k32 = 0xFFFFFFFEull;
+  uint64_t k32 = kDepthCulled - 1;
   if (r.keep) {
-    const uint64_t d = (full - p.near_bits) >> 24;
-    k32 = d < 0xFFFFFFFEull ? d : 0xFFFFFFFEull;
+    const uint64_t d = (full - p.near_bits) >> 32;
+    k32 = d < kDepthCulled - 1 ? d : kDepthCulled - 1;
   }
-  p.dkey32[id] = r.keep ? (uint32_t)k32 : 0xFFFFFFFFu;
+  p.dkey32[id] = r.keep ? (uint32_t)k32 : kDepthCulled;
   p.ids[id] = id;
   // Tile binning by the test box (reference rect ∩ alpha-cut ellipse box):
   // a strictly tighter, conservative version of _tile_lists' rect binning
@@ -205,13 +212,13 @@ __global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
 // S1b: runs of equal 32-bit depth keys leave the stable sort in id order;
 // sort each run by (full fp64 key, id) — runs are rare and short for real
 // scenes (one thread per run, insertion sort; already-sorted runs cost one
-// scan). The culled tail (key 0xFFFFFFFF) stays in id order.
+// scan). The culled tail (key kDepthCulled) stays in id order.
 __global__ void k_fix_runs(int32_t P, const uint32_t* __restrict__ k32,
                            const uint64_t* __restrict__ k64, int32_t* __restrict__ ids) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P - 1) return;
   const uint32_t k = k32[i];
-  if (k == 0xFFFFFFFFu || k32[i + 1] != k || (i > 0 && k32[i - 1] == k)) return;
+  if (k == kDepthCulled || k32[i + 1] != k || (i > 0 && k32[i - 1] == k)) return;
   int end = i + 1;
   while (end + 1 < P && k32[end + 1] == k) ++end;
   for (int a = i + 1; a <= end; ++a) {
@@ -952,7 +959,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
 
     TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, ws_ptr<uint32_t>(ws, L.dk32_in),
                                              ws_ptr<uint32_t>(ws, L.dk32_out), ids_in, ids_out,
-                                             P, 0, 32, st));
+                                             P, 0, kDepthKeyBits, st));
     k_fix_runs<<<(P + 255) / 256, 256, 0, st>>>(P, ws_ptr<uint32_t>(ws, L.dk32_out), dk_in,
                                                 ids_out);
     TSB_CHECK_LAUNCH("k_fix_runs");
