@@ -59,12 +59,17 @@ def main(lpath, rpath, out):
     # last frame: from the last k_preprocess to the end
     starts = [i for i, (_, n, _) in enumerate(ls) if "k_preprocess" in n]
     frame = ls[starts[-1]:] if starts else ls
+    ends = [i for i, (_, n, _) in enumerate(frame) if "k_shade" in n]
+    if ends:
+        frame = frame[:ends[0] + 1]
     tot = sum(t for _, _, t in frame)
     lines += ["## Launch list of one cfg2 frame (cold-cache, serialised; compare shares)", "",
               "| kernel | ns | share |", "|---|---:|---:|"]
     agg = OrderedDict()
     for _, n, t in frame:
         key = n.split("(")[0].replace("void ", "")[:60]
+        if key in agg and not key.startswith("tsb::"):
+            key = key + " #" + str(sum(1 for k in agg if k.startswith(key)) + 1)
         agg[key] = agg.get(key, 0.0) + t
     for k, t in agg.items():
         lines.append(f"| `{k}` | {t:.0f} | {100 * t / tot:.1f}% |")
