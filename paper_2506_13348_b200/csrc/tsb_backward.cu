@@ -336,10 +336,19 @@ struct RasterBwdParams {
   const int32_t* tile_order;
 };
 
+// Warp-private shared memory of the backward rasterizer (11 KB).
 struct BwdWarpSmem {
-  GeomRec geom[32];
-  MatRec mat[32];
-  float m[32][9];
+  DecRec dec[32];          // staged step: decide records (AoS, broadcast reads)
+  int32_t sid[32];         // splat ids
+  float lin[11][32];       // intersection forms L0..L10 (SoA)
+  float frame[9][32];      // t_u, t_v, t_u x t_v
+  float lind[3][32];       // clamped SH radiance
+  int32_t loff[32];        // chart offset in the linear atlas
+  float mf[9][32];         // float M rows 0,1,2 x cols 0,1,3 (intersection adjoint)
+  // reduction rows: first the per-splat terms of the live lanes (stride 28,
+  // compacted), then per lane the 28 weighted texel values + cell offsets
+  // (stride 36: conflict-free 128-bit stores)
+  float red[32 * 36];
 };
 
 // Decode-normal adjoint (textures.py:290-322).
@@ -363,14 +372,16 @@ __device__ __forceinline__ void decode_grad(float ea, float eb, float gx, float 
   denc[1] = 2.0f * dpy;
 }
 
-__global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
-  __shared__ BwdWarpSmem s_ws[8];
+__global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  BwdWarpSmem& ws = s_ws[warp];
+  BwdWarpSmem& ws = *reinterpret_cast<BwdWarpSmem*>(s_raw + (size_t)warp * sizeof(BwdWarpSmem));
+  const uint32_t lt_mask = (1u << lane) - 1u;
   const int TILE = p.tile;
   const int wx = TILE / 8;
   const int nblk = TILE * TILE / 32;
   const int T = p.T;
+  const int t_corner = lane / 7, t_ch = lane % 7;  // texel reducer lanes 0..27
   // persistent warps over (tile, 8x4 block) units, heaviest tiles first
   // (the forward's schedule order, left in the workspace)
   const int num_units = p.num_tiles * nblk;
@@ -382,16 +393,16 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
     const int tile = p.tile_order ? p.tile_order[unit / nblk] : unit / nblk;
     const int blk = unit % nblk;
     const int start = p.ranges[2 * tile];
-    {
     const int bx0 = (tile % p.tiles_x) * TILE + (blk % wx) * 8;
     const int by0 = (tile / p.tiles_x) * TILE + (blk / wx) * 4;
     if (bx0 >= p.W || by0 >= p.H) continue;
+    const int bx1 = min(bx0 + 8, p.W), by1 = min(by0 + 4, p.H);
     const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
     const bool inside = px < p.W && py < p.H;
     const int pix = py * p.W + px;
     const float x = (float)tsb_pixel_x(&p.cam, px), y = (float)tsb_pixel_y(&p.cam, py);
     const size_t HW = (size_t)p.W * p.H;
-    int last = inside ? p.last_entry[pix] : -1;
+    const int last = inside ? p.last_entry[pix] : -1;
     float Tc = inside ? p.T_last[pix] : 0.f;
     float g[13], R[13];
 #pragma unroll
@@ -404,49 +415,62 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
     for (int hi = blk_last; hi >= start; hi -= 32) {
       const int lo = max(start, hi - 31);
       const int cnt = hi - lo + 1;
+      // ---- stage the step [lo, hi]
       __syncwarp();
+      bool hit = false;
       if (lane < cnt) {
-        const int e = lo + lane;
-        const int id = __ldg(p.evals + e);
-        ws.geom[lane] = p.geom[id];
-        ws.mat[lane] = p.mat[id];
+        const int id = __ldg(p.evals + lo + lane);
+        hit = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, ws.lin) != 0;
+        ws.sid[lane] = id;
+        const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
+        const float4 m0 = __ldg(mq), m1 = __ldg(mq + 1), m2 = __ldg(mq + 2), m3 = __ldg(mq + 3);
+        ws.frame[0][lane] = m0.x; ws.frame[1][lane] = m0.y; ws.frame[2][lane] = m0.z;
+        ws.frame[3][lane] = m0.w; ws.frame[4][lane] = m1.x; ws.frame[5][lane] = m1.y;
+        ws.frame[6][lane] = m1.z; ws.frame[7][lane] = m1.w; ws.frame[8][lane] = m2.x;
+        ws.lind[0][lane] = m2.y; ws.lind[1][lane] = m2.z; ws.lind[2][lane] = m2.w;
+        ws.loff[lane] = __float_as_int(m3.w);
         const double* m64 = p.m64 + (size_t)kM64Stride * id;
 #pragma unroll
-        for (int c = 0; c < 9; ++c) ws.m[lane][c] = (float)m64[c];
+        for (int c = 0; c < 9; ++c) ws.mf[c][lane] = (float)__ldg(m64 + c);
       }
+      const uint32_t cand = __ballot_sync(0xffffffffu, hit);
       __syncwarp();
-      for (int k = cnt - 1; k >= 0; --k) {
-        const int e = lo + k;
-        const GeomRec& gr = ws.geom[k];
-        bool live = false;
-        float u = 0.f, v = 0.f, z = 0.f, a = 0.f;
-        if (e <= last) {
-          const int bxl = gr.bx & 0xFFFF, bxh = gr.bx >> 16, byl = gr.by & 0xFFFF, byh = gr.by >> 16;
-          if (px >= bxl && px < bxh && py >= byl && py < byh) {
-            int r = tsb_eval_lin(gr.lin, x, y, p.near_f, &u, &v, &z, &a);
-            if (r == 2) {
-              const double* m64 = p.m64 + (size_t)kM64Stride * gr.id;
-              r = tsb_live_f64(m64, m64[9], tsb_pixel_x(&p.cam, px), tsb_pixel_y(&p.cam, py),
-                               p.cam.near_z);
-            }
-            live = r != 0;
-          }
-        }
-        if (!__any_sync(0xffffffffu, live)) continue;
-        float c_acc[32];
+      if (!cand) continue;
+      // ---- decide: this pixel's contributors in the step (entries <= last)
+      uint32_t live = 0;
+      if (last >= lo) {
+        const int nv = last - lo + 1;
+        const uint32_t valid = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
+        // uniform candidate loop (broadcast reads), masked afterwards
+        live = tsb_decide_step(ws.dec, ws.lin, ws.sid, cand, lane, x, y, p.near_f, p.cam, p.m64,
+                               px, py) & valid;
+      }
+      // ---- adjoint, back to front over the entries with a live pixel
+      for (uint32_t any = __reduce_or_sync(0xffffffffu, live); any;) {
+        const int k = 31 - __clz(any);
+        any &= ~(1u << k);
+        const bool lk = (live >> k) & 1u;
+        const uint32_t lm = __ballot_sync(0xffffffffu, lk);
+        const int id = ws.sid[k];
+        int tkey = -1 - lane;  // non-live lanes: singleton groups, never leaders
+        int tdx = 0, tdy = 0;
+        float tw[28];          // texel gradient: 4 corners x 7 channels
+        if (lk) {
+          float c_acc[24];
+          float L[11];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) c_acc[c] = 0.f;
-        int tx_key = -1;
-        float tx_fs = 0.f, tx_ft = 0.f, tx_up[7];
+          for (int c = 0; c < 11; ++c) L[c] = ws.lin[c][k];
+          float u, v, z, a;
+          tsb_uvza_lin(L, x, y, &u, &v, &z, &a);
+          float fr[9];
 #pragma unroll
-        for (int c = 0; c < 7; ++c) tx_up[c] = 0.f;
-        const MatRec& m = ws.mat[k];
-        if (live) {
+          for (int c = 0; c < 9; ++c) fr[c] = ws.frame[c][k];
           // ---- recompute the fragment's attributes (verify sampler)
           tsb_texc tc;
           tsb_texel_coords(u, v, T, &tc);
           const int S = p.tstride;
-          const int r0 = m.lin_off + tc.j0 * p.page_w, r1 = m.lin_off + tc.j1 * p.page_w;
+          const int loff = ws.loff[k];
+          const int r0 = loff + tc.j0 * p.page_w, r1 = loff + tc.j1 * p.page_w;
           const float4 a00 = __ldg(p.fam_a + S * (r0 + tc.i0)), a01 = __ldg(p.fam_a + S * (r0 + tc.i1));
           const float4 a10 = __ldg(p.fam_a + S * (r1 + tc.i0)), a11 = __ldg(p.fam_a + S * (r1 + tc.i1));
           const float4 b00 = __ldg(p.fam_b + S * (r0 + tc.i0)), b01 = __ldg(p.fam_b + S * (r0 + tc.i1));
@@ -461,8 +485,8 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
           for (int c = 0; c < 7; ++c) t7[c] = tsb_lerp4(c00[c], c01[c], c10[c], c11[c], tc.fs, tc.ft);
           float xa[13];
           xa[0] = t7[0]; xa[1] = t7[1]; xa[2] = t7[2]; xa[3] = t7[4]; xa[4] = t7[3];
-          tsb_decode_normal(t7[5], t7[6], m.frame, xa + 5);
-          xa[8] = m.l_ind[0]; xa[9] = m.l_ind[1]; xa[10] = m.l_ind[2];
+          tsb_decode_normal(t7[5], t7[6], fr, xa + 5);
+          xa[8] = ws.lind[0][k]; xa[9] = ws.lind[1][k]; xa[10] = ws.lind[2][k];
           xa[11] = z;
           xa[12] = 1.0f;
           // transmittance in front of this fragment
@@ -494,7 +518,6 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
             nt[0] = nx; nt[1] = ny; nt[2] = sqrtf(q > 0.0f ? q : 0.0f);
           }
           const float dnw[3] = {dx[5], dx[6], dx[7]};
-          const float* fr = m.frame;
           const float gx = dnw[0] * fr[0] + dnw[1] * fr[1] + dnw[2] * fr[2];
           const float gy = dnw[0] * fr[3] + dnw[1] * fr[4] + dnw[2] * fr[5];
           const float gz = dnw[0] * fr[6] + dnw[1] * fr[7] + dnw[2] * fr[8];
@@ -507,11 +530,6 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
           float denc[2];
           decode_grad(t7[5], t7[6], gx, gy, gz, denc);
           const float up7[7] = {dx[0], dx[1], dx[2], dx[4], dx[3], denc[0], denc[1]};
-          // ---- texel gradients: kept per lane, scattered below per cell group
-          tx_key = tc.j0 * T + tc.i0;
-          tx_fs = tc.fs; tx_ft = tc.ft;
-#pragma unroll
-          for (int c = 0; c < 7; ++c) tx_up[c] = up7[c];
           float dfs = 0.f, dft = 0.f;
 #pragma unroll
           for (int c = 0; c < 7; ++c) {
@@ -534,7 +552,9 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
           }
           // ---- intersection adjoint (rasterize.py:605-639), fold to dWH
           {
-            const float* M = ws.m[k];  // rows 0,1,2 x cols 0,1,3
+            float M[9];
+#pragma unroll
+            for (int c = 0; c < 9; ++c) M[c] = ws.mf[c][k];  // rows 0,1,2 x cols 0,1,3
             const float hu0 = x * M[6] - M[0], hu1 = x * M[7] - M[1], hu3 = x * M[8] - M[2];
             const float hv0 = y * M[6] - M[3], hv1 = y * M[7] - M[4], hv3 = y * M[8] - M[5];
             const float D = hu0 * hv1 - hu1 * hv0;
@@ -553,46 +573,65 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterBwdParams p) {
             c_acc[7] = dz * vv + (x * dhu1 + y * dhv1);
             c_acc[8] = dz + (x * dhu3 + y * dhv3);
           }
-        }
-        // ---- warp-reduce the 22 per-splat terms (lane c ends with term c)
-        const float tot = warp_transpose_reduce(c_acc, lane);
-        if (lane < 22 && tot != 0.0f) atomicAdd(p.acc + (size_t)kAccWords * gr.id + lane, tot);
-        // ---- texel gradients (per-splat (T, T, 7) combined layout,
-        // rasterize.py:548-562): lanes hitting the same bilinear cell are
-        // reduced together (28 values: 4 corners x 7 channels), one
-        // 28-lane atomic per cell group
-        {
-          float* dt = p.dtexels + (size_t)gr.id * T * T * 7;
-          uint32_t pending = __ballot_sync(0xffffffffu, tx_key >= 0);
-          while (pending) {
-            const int key = __shfl_sync(0xffffffffu, tx_key, __ffs(pending) - 1);
-            const bool in = tx_key == key;
-            pending &= ~__ballot_sync(0xffffffffu, in);
-            float v[32];
-            const float w00 = (1.0f - tx_fs) * (1.0f - tx_ft), w01 = tx_fs * (1.0f - tx_ft);
-            const float w10 = (1.0f - tx_fs) * tx_ft, w11 = tx_fs * tx_ft;
+          c_acc[22] = c_acc[23] = 0.f;
+          // ---- per-splat terms: row at the lane's rank among the live lanes
+          float4* rr = reinterpret_cast<float4*>(ws.red + 28 * __popc(lm & lt_mask));
 #pragma unroll
-            for (int c = 0; c < 7; ++c) {
-              v[c] = in ? tx_up[c] * w00 : 0.f;
-              v[7 + c] = in ? tx_up[c] * w01 : 0.f;
-              v[14 + c] = in ? tx_up[c] * w10 : 0.f;
-              v[21 + c] = in ? tx_up[c] * w11 : 0.f;
-            }
-            v[28] = v[29] = v[30] = v[31] = 0.f;
-            const float tsum = warp_transpose_reduce(v, lane);
+          for (int q = 0; q < 6; ++q)
+            rr[q] = make_float4(c_acc[4 * q], c_acc[4 * q + 1], c_acc[4 * q + 2], c_acc[4 * q + 3]);
+#pragma unroll
+          for (int c = 0; c < 7; ++c) {
+            tw[c] = up7[c] * ((1.0f - tc.fs) * (1.0f - tc.ft));
+            tw[7 + c] = up7[c] * (tc.fs * (1.0f - tc.ft));
+            tw[14 + c] = up7[c] * ((1.0f - tc.fs) * tc.ft);
+            tw[21 + c] = up7[c] * (tc.fs * tc.ft);
+          }
+          // cell key = the (i0, j0) corner's offset; corner steps to (i1, j1)
+          tkey = 7 * (tc.j0 * T + tc.i0);
+          tdx = 7 * (tc.i1 - tc.i0);
+          tdy = 7 * T * (tc.j1 - tc.j0);
+        }
+        __syncwarp();
+        // ---- per-splat terms: lane c < 22 sums column c over the live rows
+        if (lane < 22) {
+          const int nl = __popc(lm);
+          float tot = 0.f;
+          for (int i = 0; i < nl; ++i) tot += ws.red[28 * i + lane];
+          if (tot != 0.0f) atomicAdd(p.acc + (size_t)kAccWords * id + lane, tot);
+        }
+        __syncwarp();
+        if (lk) {
+          float4* tr = reinterpret_cast<float4*>(ws.red + 36 * lane);
+#pragma unroll
+          for (int q = 0; q < 7; ++q)
+            tr[q] = make_float4(tw[4 * q], tw[4 * q + 1], tw[4 * q + 2], tw[4 * q + 3]);
+          tr[7] = make_float4(__int_as_float(tkey), __int_as_float(tdx), __int_as_float(tdy), 0.f);
+        }
+        __syncwarp();
+        // ---- texel gradients (per-splat (T, T, 7) combined layout,
+        // rasterize.py:548-562): live lanes grouped by bilinear cell
+        // (match.any); for each group, reducer lane (corner, channel) sums
+        // its weighted value over the members and issues one atomic
+        {
+          float* dt = p.dtexels + (size_t)id * T * T * 7;
+          const uint32_t peers = __match_any_sync(0xffffffffu, tkey);
+          uint32_t leaders = __ballot_sync(0xffffffffu, lk && lane == __ffs(peers) - 1);
+          while (leaders) {
+            const int l = __ffs(leaders) - 1;
+            leaders &= leaders - 1;
+            const uint32_t grp = __shfl_sync(0xffffffffu, peers, l);
             if (lane < 28) {
-              const int i0 = key % T, j0 = key / T;
-              const int i1 = i0 + 1 < T - 1 ? i0 + 1 : T - 1;
-              const int j1 = j0 + 1 < T - 1 ? j0 + 1 : T - 1;
-              const int corner = lane / 7, ch = lane % 7;
-              const int ii = (corner & 1) ? i1 : i0, jj = (corner & 2) ? j1 : j0;
-              if (tsum != 0.0f) atomicAdd(dt + 7 * (jj * T + ii) + ch, tsum);
+              float tsum = 0.f;
+              for (uint32_t m = grp; m; m &= m - 1) tsum += ws.red[36 * (__ffs(m) - 1) + lane];
+              const int* lr = reinterpret_cast<const int*>(ws.red + 36 * l + 28);
+              const int off = lr[0] + ((t_corner & 1) ? lr[1] : 0) + ((t_corner & 2) ? lr[2] : 0) + t_ch;
+              if (tsum != 0.0f) atomicAdd(dt + off, tsum);
             }
           }
         }
+        __syncwarp();
       }
     }
-  }
   }
 }
 
@@ -881,15 +920,19 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera, const 
   rp.work_counter = reinterpret_cast<int32_t*>(const_cast<int64_t*>(ws_ptr<int64_t>(ws, L.counters)) + 2);
   rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);
   TSB_CUDA(cudaMemsetAsync(rp.work_counter, 0, 4, st));
+  const size_t smem = 8 * sizeof(BwdWarpSmem);
   static int resident = 0;
   if (!resident) {
     int dev = 0, sms = 0, per_sm = 0;
+    TSB_CUDA(cudaFuncSetAttribute(k_raster_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     TSB_CUDA(cudaGetDevice(&dev));
     TSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_bwd, 256, 0));
+    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_bwd, 256, smem));
     resident = sms * (per_sm > 0 ? per_sm : 1);
   }
-  k_raster_bwd<<<std::min(L.num_tiles, resident), 256, 0, st>>>(rp);
+  const int units = L.num_tiles * (tile * tile / 32);
+  k_raster_bwd<<<std::min((units + 7) / 8, resident), 256, smem, st>>>(rp);
   TSB_CHECK_LAUNCH("k_raster_bwd");
   FinishParams fp;
   fp.cam = to_cam(camera);

@@ -415,23 +415,11 @@ __device__ __forceinline__ float frag_composite(const MatRec& m, const Frag& f, 
   return tsb_composite(acc, xa, f.a, T);
 }
 
-#ifndef TSB_DECIDE_ILP
-#define TSB_DECIDE_ILP 2
-#endif
 #ifndef TSB_PAIR_ILP
 #define TSB_PAIR_ILP 2
 #endif
 
 // Warp-private shared memory of the rasterizer.
-// What the decide loop reads of one staged splat: 48 bytes, three
-// broadcast 128-bit loads (a 48-byte lane stride also makes the staging
-// stores conflict-free).
-struct __align__(16) DecRec {
-  float lin[10];      // L0..L9: D, Nu, Nv forms and det
-  float r2hi;         // L11
-  uint32_t pixmask;   // pixels of the current 8x4 block inside the test box
-};
-
 struct WarpSmem {
   // staged step, AoS for the decide loop (all lanes read the same splat)
   DecRec dec[32];
@@ -596,30 +584,9 @@ k_raster_fwd(RasterParams p) {
       __syncwarp();
       if (e < end) {
         const int id = __ldg(p.evals + e);
-        const float4* gq = reinterpret_cast<const float4*>(p.geom + id);
-        const float4 gv[4] = {__ldg(gq), __ldg(gq + 1), __ldg(gq + 2), __ldg(gq + 3)};
-        // test box -> mask of this block's pixels inside it
-        const uint32_t gbx = __float_as_uint(gv[3].x), gby = __float_as_uint(gv[3].y);
-        const int cx0 = min(max((int)(gbx & 0xFFFF) - bx0, 0), 8);
-        const int cx1 = min(max((int)(gbx >> 16) - bx0, 0), bx1 - bx0);
-        const int cy0 = min(max((int)(gby & 0xFFFF) - by0, 0), 4);
-        const int cy1 = min(max((int)(gby >> 16) - by0, 0), by1 - by0);
-        uint32_t pm = 0;
-        if (cx1 > cx0 && cy1 > cy0) {
-          const uint32_t row = ((1u << cx1) - 1u) & ~((1u << cx0) - 1u);
-          const uint32_t rows = (uint32_t)(((1ull << (8 * cy1)) - 1ull) & ~((1ull << (8 * cy0)) - 1ull));
-          pm = (row * 0x01010101u) & rows;
-        }
+        const uint32_t pm = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, ws.lin);
         hit = pm != 0;
-        float4* d = reinterpret_cast<float4*>(&ws.dec[lane]);
-        d[0] = gv[0];
-        d[1] = gv[1];
-        d[2] = make_float4(gv[2].x, gv[2].y, gv[2].w, __uint_as_float(pm));
         ws.sid[lane] = id;
-        const float gl[11] = {gv[0].x, gv[0].y, gv[0].z, gv[0].w, gv[1].x, gv[1].y,
-                              gv[1].z, gv[1].w, gv[2].x, gv[2].y, gv[2].z};
-#pragma unroll
-        for (int c = 0; c < 11; ++c) ws.lin[c][lane] = gl[c];
         const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
         const float4 m0 = __ldg(mq), m1 = __ldg(mq + 1), m2 = __ldg(mq + 2), m3 = __ldg(mq + 3);
         ws.frame[0][lane] = m0.x; ws.frame[1][lane] = m0.y; ws.frame[2][lane] = m0.z;
@@ -634,42 +601,9 @@ k_raster_fwd(RasterParams p) {
       if (!cand) continue;
       // ---- decide
       uint32_t live = 0;
-      if (!done) {
-        // TSB_DECIDE_ILP candidates per iteration, predicated (independent chains)
-        uint32_t undecided = 0;
-        for (uint32_t m = cand; m;) {
-          int kk[TSB_DECIDE_ILP];
-#pragma unroll
-          for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
-            kk[j] = m ? __ffs(m) - 1 : kk[0];
-            m &= m - 1;
-          }
-#pragma unroll
-          for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
-            const DecRec& g = ws.dec[kk[j]];
-            const bool in = (g.pixmask >> lane) & 1u;
-            const int r = tsb_predecide_lin_nb(g.lin, g.r2hi, x, y, p.near_f);
-            live |= (in && r == 1 ? 1u : 0u) << kk[j];
-            undecided |= (in && r == 2 ? 1u : 0u) << kk[j];
-          }
-        }
-        // the rare candidates near the alpha cut / near plane: exact path
-        for (uint32_t m = undecided; m; m &= m - 1) {
-          const int k = __ffs(m) - 1;
-          float L[12];
-#pragma unroll
-          for (int c = 0; c < 11; ++c) L[c] = ws.lin[c][k];
-          L[11] = ws.dec[k].r2hi;
-          float u, v, z, a;
-          int r = tsb_eval_lin(L, x, y, p.near_f, &u, &v, &z, &a);
-          if (r == 2) {
-            const double* m64 = p.m64 + (size_t)kM64Stride * ws.sid[k];
-            r = tsb_live_f64(m64, m64[9], tsb_pixel_x(&p.cam, px), tsb_pixel_y(&p.cam, py),
-                             p.cam.near_z);
-          }
-          if (r) live |= 1u << k;
-        }
-      }
+      if (!done)
+        live = tsb_decide_step(ws.dec, ws.lin, ws.sid, cand, lane, x, y, p.near_f, p.cam, p.m64,
+                               px, py);
       // ---- texture + blend, in order, TSB_PAIR_ILP live pairs per lane per iteration
       while (__any_sync(0xffffffffu, live != 0)) {
         if (live) {
