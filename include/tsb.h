@@ -184,8 +184,15 @@ typedef struct tsb_scene_grads {
   double* scales;      /* P x 2 */
   double* opacities;   /* P     */
   double* sh;          /* P x K x 3 */
-  float* texels;       /* P x T x T x 7 */
+  float* texels;       /* P x T x T x 7 (combined order), or x 8 (interleaved) */
+  int32_t texel_layout; /* TSB_TEXELS_COMBINED (the reference's per-splat
+                           [alb rgb, rough, metal, nrm a, nrm b]) or
+                           TSB_TEXELS_INTERLEAVED (the 8-channel atlas order
+                           [alb rgb, rough, nrm a, nrm b, metal, 0]) */
 } tsb_scene_grads;
+
+#define TSB_TEXELS_COMBINED 0
+#define TSB_TEXELS_INTERLEAVED 1
 
 /* environment.py:198-206 EnvGrads, float32, accumulated into. */
 typedef struct tsb_env_grads {
@@ -221,6 +228,63 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera,
                         uint64_t workspace_bytes, int64_t max_entries,
                         const tsb_pixel_state* pixels, const float* dgbuf, void* scratch,
                         tsb_scene_grads* grads, void* stream);
+
+/* ---- Training-step glue (K10-K13) ------------------------------------- */
+
+/* Scratch bytes of tsb_loss_image for a W x H image. */
+int tsb_loss_scratch_size(int32_t width, int32_t height, uint64_t* bytes);
+
+/* K10: image loss of a training step (replaces losses.image_loss
+ * losses.py:120-134 composed with linear_to_display / _grad :24-37 as in
+ * compute_step training.py:143-146). color: linear H x W x 3 (the shaded
+ * image), target: display-space H x W x 3. Writes dcolor (H x W x 3) =
+ * d loss / d color and ADDS into terms (device doubles, zero them first):
+ * terms[0] += sum |disp - target|, terms[1] += sum SSIM map,
+ * terms[2] += sum (clip(disp) - clip(target))^2 (for PSNR); each over the
+ * 3 W H values. loss_image = (1-w) terms[0]/N + w (1 - terms[1]/N)/2. */
+int tsb_loss_image(const float* color, const float* target, int32_t width, int32_t height,
+                   float dssim_weight, float* dcolor, double* terms, void* scratch,
+                   uint64_t scratch_bytes, void* stream);
+
+/* K11: normal-consistency and smoothness regularisers of compute_step
+ * (training.py:147-172; losses.py:147-277). gbuf: planar 13 x H x W G-buffer
+ * of the step, target: display H x W x 3. ADDS their gradients into the
+ * planar dgbuf (normal channels 5..7, depth 11, alpha 12) and into terms:
+ * terms[3] += sum (1 - n.n_ref) and terms[4] += count over valid pixels,
+ * terms[5] += sum w |dn| and terms[6] += pair count (the losses are
+ * terms[3]/max(terms[4],1) and terms[5]/max(terms[6],1)). */
+int tsb_loss_regularizers(const float* gbuf, const float* target, const tsb_camera* camera,
+                          float normal_weight, float smooth_weight, float* dgbuf, double* terms,
+                          void* stream);
+
+/* K12: one Adam step (training.py:69-100 Adam.step) over up to
+ * TSB_ADAM_MAX_GROUPS parameter groups in one launch, each followed by its
+ * projection (clip to [0,1] or a floor, training.py:270-293). Gradients are
+ * float32; parameters and moments are float32 or float64 (dtype). */
+#define TSB_ADAM_MAX_GROUPS 24
+#define TSB_F32 0
+#define TSB_F64 1
+#define TSB_CLAMP_NONE 0
+#define TSB_CLAMP_UNIT 1
+#define TSB_CLAMP_FLOOR 2
+typedef struct tsb_adam_group {
+  void* param;          /* count elements of dtype */
+  const float* grad;    /* count float32 */
+  void* m;              /* first moment, dtype */
+  void* v;              /* second moment, dtype */
+  int64_t count;
+  double lr;
+  double floor;         /* TSB_CLAMP_FLOOR */
+  int32_t dtype;
+  int32_t clamp;
+} tsb_adam_group;
+int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step, double beta1,
+                  double beta2, double eps, void* stream);
+
+/* K13: Gram-Schmidt re-orthonormalisation of the tangent frames
+ * (Scene.renormalize_tangents, splats.py:382-392), in place, float64. */
+int tsb_orthonormalize_tangents(int32_t num_splats, double* tangent_u, double* tangent_v,
+                                void* stream);
 
 /* Last error message of the calling thread. */
 const char* tsb_last_error(void);

@@ -65,7 +65,22 @@ class PixelState_t(C.Structure):
 class SceneGrads_t(C.Structure):
     _fields_ = [("positions", C.c_void_p), ("tangent_u", C.c_void_p),
                 ("tangent_v", C.c_void_p), ("scales", C.c_void_p),
-                ("opacities", C.c_void_p), ("sh", C.c_void_p), ("texels", C.c_void_p)]
+                ("opacities", C.c_void_p), ("sh", C.c_void_p), ("texels", C.c_void_p),
+                ("texel_layout", C.c_int32)]
+
+
+TEXELS_COMBINED = 0
+TEXELS_INTERLEAVED = 1
+
+ADAM_MAX_GROUPS = 24
+F32, F64 = 0, 1
+CLAMP_NONE, CLAMP_UNIT, CLAMP_FLOOR = 0, 1, 2
+
+
+class AdamGroup_t(C.Structure):
+    _fields_ = [("param", C.c_void_p), ("grad", C.c_void_p), ("m", C.c_void_p),
+                ("v", C.c_void_p), ("count", C.c_int64), ("lr", C.c_double),
+                ("floor", C.c_double), ("dtype", C.c_int32), ("clamp", C.c_int32)]
 
 
 class EnvGrads_t(C.Structure):
@@ -98,6 +113,12 @@ _SIGNATURES = {
                             C.c_int32, _P, C.c_uint64, C.c_int64, C.POINTER(PixelState_t), _P,
                             _P, C.POINTER(SceneGrads_t), _P],
     "tsb_backward_scratch_size": [C.c_int32, C.POINTER(C.c_uint64)],
+    "tsb_loss_scratch_size": [C.c_int32, C.c_int32, C.POINTER(C.c_uint64)],
+    "tsb_loss_image": [_P, _P, C.c_int32, C.c_int32, C.c_float, _P, _P, _P, C.c_uint64, _P],
+    "tsb_loss_regularizers": [_P, _P, C.POINTER(Camera_t), C.c_float, C.c_float, _P, _P, _P],
+    "tsb_adam_step": [C.POINTER(AdamGroup_t), C.c_int32, C.c_int32, C.c_double, C.c_double,
+                      C.c_double, _P],
+    "tsb_orthonormalize_tangents": [C.c_int32, _P, _P, _P],
 }
 
 _lib = None

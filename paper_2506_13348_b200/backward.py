@@ -35,7 +35,9 @@ class SceneGrads:
     scales: torch.Tensor      # (P, 2) float64
     opacities: torch.Tensor   # (P,) float64
     sh: torch.Tensor          # (P, K, 3) float64
-    texels_dense: torch.Tensor  # (P, T, T, 7) float32, combined order
+    texels_dense: torch.Tensor  # (P, T, T, 7) float32, combined order (or (P, T, T, 8)
+    #                             interleaved atlas order when texel_layout == 1)
+    texel_layout: int = 0
 
     @staticmethod
     def zeros(P, K, T, device):
@@ -48,7 +50,10 @@ class SceneGrads:
     @property
     def texels(self):
         """Reference-style list: (T, T, 7) per splat, None if untouched."""
-        t = self.texels_dense.cpu().numpy().astype(np.float64)
+        t = self.texels_dense
+        if self.texel_layout == _lib.TEXELS_INTERLEAVED:
+            t = t[..., [0, 1, 2, 3, 6, 4, 5]]
+        t = t.cpu().numpy().astype(np.float64)
         touched = np.any(t != 0, axis=(1, 2, 3))
         return [t[k] if touched[k] else None for k in range(t.shape[0])]
 
@@ -61,6 +66,7 @@ class SceneGrads:
         s.opacities = _lib.ptr(self.opacities)
         s.sh = _lib.ptr(self.sh)
         s.texels = _lib.ptr(self.texels_dense)
+        s.texel_layout = self.texel_layout
         return s
 
     def flat(self) -> list:
@@ -134,10 +140,13 @@ class DeviceEnvGrads:
                         self.diffuse.double().cpu().numpy())
 
 
-def shade_backward(result: ShadeResult, camera, env, lut, dcolor):
+def shade_backward(result: ShadeResult, camera, env, lut, dcolor, *, env_grads=None,
+                   dgbuf=None):
     """Backpropagate a gradient on ShadeResult.color (shading.py:186-228).
 
-    Returns (dgbuf planar (13, H, W) float32, DeviceEnvGrads)."""
+    Returns (dgbuf planar (13, H, W) float32, DeviceEnvGrads). `env_grads`
+    (a DeviceEnvGrads) and `dgbuf` may be preallocated; env gradients are
+    accumulated into them."""
     planar, denv_cached, bg = result.cache
     denv = denv_cached if env is None else device_environment(env, lut, planar.device)
     H, W = int(camera.height), int(camera.width)
@@ -146,8 +155,10 @@ def shade_backward(result: ShadeResult, camera, env, lut, dcolor):
     dc = dc.to(device=dev, dtype=torch.float32).contiguous()
     if tuple(dc.shape) != (H, W, 3):
         raise ValueError("dcolor must be (H, W, 3)")
-    dgbuf = torch.empty((NUM_CHANNELS, H, W), dtype=torch.float32, device=dev)
-    eg = DeviceEnvGrads([torch.zeros_like(m) for m in denv.mips], torch.zeros_like(denv.diffuse))
+    if dgbuf is None:
+        dgbuf = torch.empty((NUM_CHANNELS, H, W), dtype=torch.float32, device=dev)
+    eg = env_grads if env_grads is not None else DeviceEnvGrads(
+        [torch.zeros_like(m) for m in denv.mips], torch.zeros_like(denv.diffuse))
     bgc = (C.c_float * 3)(*[float(v) for v in np.asarray(bg, np.float64)])
     cam = _lib.camera_struct(camera)
     es = denv.struct()

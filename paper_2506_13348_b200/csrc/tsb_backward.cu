@@ -330,7 +330,8 @@ struct RasterBwdParams {
   const float* T_last;
   const float* dgbuf;
   float* acc;          // P x kAccWords
-  float* dtexels;      // P x T x T x 7
+  float* dtexels;      // P x T x T x tl
+  int32_t tl;          // channels per texel: 7 (combined) or 8 (interleaved)
   int32_t num_tiles;
   int32_t* work_counter;
   const int32_t* tile_order;
@@ -382,6 +383,10 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
   const int nblk = TILE * TILE / 32;
   const int T = p.T;
   const int t_corner = lane / 7, t_ch = lane % 7;  // texel reducer lanes 0..27
+  // combined channel -> slot of the texel layout (identity, or the 8-channel
+  // interleaved atlas order [alb rgb, rough, nrm a, nrm b, metal, 0])
+  const int t_slot = p.tl == 8 ? (t_ch == 4 ? 6 : (t_ch >= 5 ? t_ch - 1 : t_ch)) : t_ch;
+  const int tl = p.tl;
   // persistent warps over (tile, 8x4 block) units, heaviest tiles first
   // (the forward's schedule order, left in the workspace)
   const int num_units = p.num_tiles * nblk;
@@ -587,9 +592,9 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
             tw[21 + c] = up7[c] * (tc.fs * tc.ft);
           }
           // cell key = the (i0, j0) corner's offset; corner steps to (i1, j1)
-          tkey = 7 * (tc.j0 * T + tc.i0);
-          tdx = 7 * (tc.i1 - tc.i0);
-          tdy = 7 * T * (tc.j1 - tc.j0);
+          tkey = tl * (tc.j0 * T + tc.i0);
+          tdx = tl * (tc.i1 - tc.i0);
+          tdy = tl * T * (tc.j1 - tc.j0);
         }
         __syncwarp();
         // ---- per-splat terms: lane c < 22 sums column c over the live rows
@@ -613,7 +618,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
         // (match.any); for each group, reducer lane (corner, channel) sums
         // its weighted value over the members and issues one atomic
         {
-          float* dt = p.dtexels + (size_t)id * T * T * 7;
+          float* dt = p.dtexels + (size_t)id * T * T * tl;
           const uint32_t peers = __match_any_sync(0xffffffffu, tkey);
           uint32_t leaders = __ballot_sync(0xffffffffu, lk && lane == __ffs(peers) - 1);
           while (leaders) {
@@ -624,7 +629,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
               float tsum = 0.f;
               for (uint32_t m = grp; m; m &= m - 1) tsum += ws.red[36 * (__ffs(m) - 1) + lane];
               const int* lr = reinterpret_cast<const int*>(ws.red + 36 * l + 28);
-              const int off = lr[0] + ((t_corner & 1) ? lr[1] : 0) + ((t_corner & 2) ? lr[2] : 0) + t_ch;
+              const int off = lr[0] + ((t_corner & 1) ? lr[1] : 0) + ((t_corner & 2) ? lr[2] : 0) + t_slot;
               if (tsum != 0.0f) atomicAdd(dt + off, tsum);
             }
           }
@@ -916,6 +921,7 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera, const 
   rp.dgbuf = dgbuf;
   rp.acc = acc;
   rp.dtexels = grads->texels;
+  rp.tl = grads->texel_layout == TSB_TEXELS_INTERLEAVED ? 8 : 7;
   rp.num_tiles = L.num_tiles;
   rp.work_counter = reinterpret_cast<int32_t*>(const_cast<int64_t*>(ws_ptr<int64_t>(ws, L.counters)) + 2);
   rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);

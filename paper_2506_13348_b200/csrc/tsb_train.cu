@@ -1,0 +1,630 @@
+// tsb_train.cu — training-step glue for sm_100a: image loss, regularisers,
+// fused Adam and the tangent-frame projection.
+//
+//   K10 image loss      display transform (losses.py:24-37), L1 and D-SSIM
+//                       with the 11-tap separable Gaussian (losses.py:48-134)
+//                       and their adjoints (ssim_backward :103-117,
+//                       linear_to_display_grad :31-37): four passes
+//                       (horizontal / vertical blur of the five SSIM moments,
+//                       then of the three moment adjoints).
+//   K11 regularisers    normal consistency against depth-derived normals and
+//                       edge-aware normal smoothness (losses.py:147-277) with
+//                       the compute_step chain into the G-buffer
+//                       (training.py:152-172): a counting pass and a gradient
+//                       pass (the means need the global valid counts).
+//   K12 Adam            one launch over every parameter group
+//                       (training.py:69-100), with the step's projections
+//                       (opacity clip, scale floor, texel clip).
+//   K13 tangents        Gram-Schmidt re-orthonormalisation (splats.py:382-392).
+//
+// Sums are accumulated in fp64 (device atomics); per-pixel math is fp32.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "tsb_internal.cuh"
+
+namespace tsb {
+
+namespace {
+
+constexpr int kR = 5;  // SSIM window radius (11 taps, sigma 1.5)
+__constant__ float c_win[2 * kR + 1];
+constexpr float kDisplayToe = 1e-4f;
+constexpr float kGammaInv = (float)(1.0 / 2.2);
+constexpr float kSsimC1 = 0.01f * 0.01f;
+constexpr float kSsimC2 = 0.03f * 0.03f;
+
+__device__ __forceinline__ float display_of(float x) {
+  x = fmaxf(x, 0.0f);
+  const float toe_slope = powf(kDisplayToe, kGammaInv - 1.0f);
+  return x >= kDisplayToe ? powf(fmaxf(x, kDisplayToe), kGammaInv) : toe_slope * x;
+}
+
+__device__ __forceinline__ float display_slope(float x) {
+  const float toe_slope = powf(kDisplayToe, kGammaInv - 1.0f);
+  float s = x >= kDisplayToe ? kGammaInv * powf(fmaxf(x, kDisplayToe), kGammaInv - 1.0f)
+                             : toe_slope;
+  return x < 0.0f ? 0.0f : s;
+}
+
+__device__ __forceinline__ void block_sum_atomic(double v, double* dst) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v != 0.0) atomicAdd(dst, v);
+}
+
+// ---- K10 pass 1: display images, L1 / MSE sums, horizontal blur of the
+// five SSIM moments (a, b, a^2, b^2, ab) per channel -> m5[15][H][W].
+__global__ void __launch_bounds__(256) k_ssim_pass1(int W, int H, const float* __restrict__ color,
+                                                    const float* __restrict__ target,
+                                                    float* __restrict__ m5,
+                                                    double* __restrict__ terms) {
+  __shared__ float sa[3][256 + 2 * kR], sb[3][256 + 2 * kR];
+  const int y = blockIdx.y;
+  const int x0 = blockIdx.x * 256;
+  const int x = x0 + threadIdx.x;
+  for (int i = threadIdx.x; i < 256 + 2 * kR; i += 256) {
+    const int xx = x0 - kR + i;
+    const bool ok = xx >= 0 && xx < W;
+    for (int c = 0; c < 3; ++c) {
+      const size_t o = 3 * ((size_t)y * W + xx) + c;
+      sa[c][i] = ok ? display_of(color[o]) : 0.0f;
+      sb[c][i] = ok ? target[o] : 0.0f;
+    }
+  }
+  __syncthreads();
+  double l1 = 0.0, se = 0.0;
+  if (x < W) {
+    const size_t HW = (size_t)W * H, pix = (size_t)y * W + x;
+    for (int c = 0; c < 3; ++c) {
+      const float a = sa[c][threadIdx.x + kR], b = sb[c][threadIdx.x + kR];
+      l1 += fabsf(a - b);
+      const float d = fminf(fmaxf(a, 0.f), 1.f) - fminf(fmaxf(b, 0.f), 1.f);
+      se += d * d;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+#pragma unroll
+      for (int t = 0; t <= 2 * kR; ++t) {
+        const float w = c_win[t], av = sa[c][threadIdx.x + t], bv = sb[c][threadIdx.x + t];
+        s0 += w * av;
+        s1 += w * bv;
+        s2 += w * av * av;
+        s3 += w * bv * bv;
+        s4 += w * av * bv;
+      }
+      float* o = m5 + (size_t)(5 * c) * HW + pix;
+      o[0] = s0; o[HW] = s1; o[2 * HW] = s2; o[3 * HW] = s3; o[4 * HW] = s4;
+    }
+  }
+  block_sum_atomic(l1, terms + 0);
+  block_sum_atomic(se, terms + 2);
+}
+
+// ---- K10 pass 2: vertical blur of the moments, SSIM map, its sum and the
+// per-pixel moment adjoints (ssim_backward): part[9][H][W] =
+// (g_mu_a, g_saa, g_sab) per channel, already scaled by upstream / N.
+__global__ void __launch_bounds__(256) k_ssim_pass2(int W, int H, const float* __restrict__ m5,
+                                                    float* __restrict__ part, float g,
+                                                    double* __restrict__ terms) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  double msum = 0.0;
+  if (x < W) {
+    const size_t HW = (size_t)W * H, pix = (size_t)y * W + x;
+    for (int c = 0; c < 3; ++c) {
+      float mom[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int t = 0; t <= 2 * kR; ++t) {
+        const int yy = y - kR + t;
+        if (yy < 0 || yy >= H) continue;
+        const float w = c_win[t];
+        const float* src = m5 + (size_t)(5 * c) * HW + (size_t)yy * W + x;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) mom[k] += w * src[k * HW];
+      }
+      const float mu_a = mom[0], mu_b = mom[1];
+      const float saa = mom[2] - mu_a * mu_a, sbb = mom[3] - mu_b * mu_b;
+      const float sab = mom[4] - mu_a * mu_b;
+      const float p = 2.0f * mu_a * mu_b + kSsimC1, q = 2.0f * sab + kSsimC2;
+      const float r = mu_a * mu_a + mu_b * mu_b + kSsimC1, s = saa + sbb + kSsimC2;
+      const float m = (p * q) / (r * s);
+      msum += m;
+      const float rs = r * s;
+      const float g_p = g * q / rs, g_q = g * p / rs;
+      const float g_r = -g * m / r, g_s = -g * m / s;
+      const float g_sab = 2.0f * g_q, g_saa = g_s;
+      const float g_mu_a = 2.0f * mu_b * g_p + 2.0f * mu_a * g_r - mu_b * g_sab - 2.0f * mu_a * g_saa;
+      float* o = part + (size_t)(3 * c) * HW + pix;
+      o[0] = g_mu_a; o[HW] = g_saa; o[2 * HW] = g_sab;
+    }
+  }
+  block_sum_atomic(msum, terms + 1);
+}
+
+// ---- K10 pass 3: horizontal blur of the 9 adjoint planes.
+__global__ void __launch_bounds__(256) k_ssim_pass3(int W, int H, const float* __restrict__ part,
+                                                    float* __restrict__ out) {
+  __shared__ float sp[256 + 2 * kR];
+  const int y = blockIdx.y, plane = blockIdx.z;
+  const int x0 = blockIdx.x * 256, x = x0 + threadIdx.x;
+  const size_t HW = (size_t)W * H;
+  const float* src = part + plane * HW + (size_t)y * W;
+  for (int i = threadIdx.x; i < 256 + 2 * kR; i += 256) {
+    const int xx = x0 - kR + i;
+    sp[i] = (xx >= 0 && xx < W) ? src[xx] : 0.0f;
+  }
+  __syncthreads();
+  if (x >= W) return;
+  float s = 0.f;
+#pragma unroll
+  for (int t = 0; t <= 2 * kR; ++t) s += c_win[t] * sp[threadIdx.x + t];
+  out[plane * HW + (size_t)y * W + x] = s;
+}
+
+// ---- K10 pass 4: vertical blur of the adjoints and the colour gradient:
+// d(pred) = (1-w) sign(a-b)/N + blur(g_mu_a) + 2a blur(g_saa) + b blur(g_sab),
+// dcolor = d(pred) * display'(color).
+__global__ void __launch_bounds__(256) k_ssim_pass4(int W, int H, const float* __restrict__ hb,
+                                                    const float* __restrict__ color,
+                                                    const float* __restrict__ target,
+                                                    float l1_scale, float* __restrict__ dcolor) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= W) return;
+  const size_t HW = (size_t)W * H, pix = (size_t)y * W + x;
+  for (int c = 0; c < 3; ++c) {
+    float v[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t <= 2 * kR; ++t) {
+      const int yy = y - kR + t;
+      if (yy < 0 || yy >= H) continue;
+      const float w = c_win[t];
+      const float* src = hb + (size_t)(3 * c) * HW + (size_t)yy * W + x;
+      v[0] += w * src[0];
+      v[1] += w * src[HW];
+      v[2] += w * src[2 * HW];
+    }
+    const float cx = color[3 * pix + c];
+    const float a = display_of(cx), b = target[3 * pix + c];
+    const float d = a - b;
+    const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+    const float dpred = l1_scale * sg + v[0] + 2.0f * a * v[1] + b * v[2];
+    dcolor[3 * pix + c] = dpred * display_slope(cx);
+  }
+}
+
+// ---- K11 regularisers ------------------------------------------------------
+struct RegParams {
+  int W, H;
+  double fx, fy, cx, cy;
+  float R[9];          // camera rotation (world_to_view[:3,:3]), row-major
+  const float* gbuf;   // 13 x H x W
+  const float* target; // H x W x 3 display
+  float* dgbuf;        // 13 x H x W (accumulated)
+  double* terms;       // [3] normal sum, [4] normal count, [5] smooth sum, [6] smooth count
+  float w_normal, w_smooth;
+};
+
+constexpr float kCoverAlpha = 0.5f;
+
+struct PixReg {
+  bool cover, n_ok;
+  float zbar, a_safe;
+  float P[3];     // back-projected view-space point
+  float n[3];     // unit normal image
+  float mag;      // |blended normal|
+};
+
+__device__ __forceinline__ PixReg reg_pixel(const RegParams& p, int x, int y) {
+  PixReg r;
+  const size_t HW = (size_t)p.W * p.H, pix = (size_t)y * p.W + x;
+  const float alpha = p.gbuf[12 * HW + pix];
+  r.cover = alpha > kCoverAlpha;
+  r.a_safe = fmaxf(alpha, 1e-30f);
+  r.zbar = r.cover ? p.gbuf[11 * HW + pix] / r.a_safe : 0.0f;
+  const float xs = (float)((((double)x + 0.5) - p.cx) / p.fx);
+  const float ys = (float)((((double)y + 0.5) - p.cy) / p.fy);
+  r.P[0] = xs * r.zbar; r.P[1] = ys * r.zbar; r.P[2] = r.zbar;
+  const float nb0 = p.gbuf[5 * HW + pix], nb1 = p.gbuf[6 * HW + pix], nb2 = p.gbuf[7 * HW + pix];
+  r.mag = sqrtf(nb0 * nb0 + nb1 * nb1 + nb2 * nb2);
+  r.n_ok = r.mag > 1e-12f;
+  const float im = 1.0f / fmaxf(r.mag, 1e-30f);
+  r.n[0] = r.n_ok ? nb0 * im : 0.f;
+  r.n[1] = r.n_ok ? nb1 * im : 0.f;
+  r.n[2] = r.n_ok ? nb2 * im : 0.f;
+  return r;
+}
+
+__device__ __forceinline__ void cross3(const float* a, const float* b, float* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// Depth-derived normal at q (depth_to_normal, losses.py:147-180): needs q,
+// q+x, q+y. Fills the view-space quantities the adjoint reuses.
+struct DepthNrm {
+  bool ok;
+  float dx[3], dy[3];
+  float unit_v[3];   // oriented unit view normal (0 if !ok)
+  float mag;
+  bool flip;
+  float n_world[3];
+};
+
+__device__ __forceinline__ DepthNrm depth_normal(const RegParams& p, const PixReg& q,
+                                                 const PixReg& qx, const PixReg& qy, bool interior) {
+  DepthNrm d;
+  float nv[3] = {0.f, 0.f, 0.f};
+  for (int i = 0; i < 3; ++i) { d.dx[i] = 0.f; d.dy[i] = 0.f; }
+  bool valid = false;
+  if (interior) {
+    for (int i = 0; i < 3; ++i) {
+      d.dx[i] = qx.P[i] - q.P[i];
+      d.dy[i] = qy.P[i] - q.P[i];
+    }
+    cross3(d.dx, d.dy, nv);
+    valid = q.cover && qx.cover && qy.cover;
+  }
+  d.flip = (nv[0] * q.P[0] + nv[1] * q.P[1] + nv[2] * q.P[2]) > 0.0f;
+  if (d.flip) { nv[0] = -nv[0]; nv[1] = -nv[1]; nv[2] = -nv[2]; }
+  d.mag = sqrtf(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+  d.ok = valid && d.mag > 1e-12f;
+  const float im = 1.0f / fmaxf(d.mag, 1e-30f);
+  for (int i = 0; i < 3; ++i) d.unit_v[i] = d.ok ? nv[i] * im : 0.f;
+  // n_world = unit_v @ R  (row vector times the rotation)
+  for (int j = 0; j < 3; ++j)
+    d.n_world[j] = d.unit_v[0] * p.R[0 * 3 + j] + d.unit_v[1] * p.R[1 * 3 + j] +
+                   d.unit_v[2] * p.R[2 * 3 + j];
+  return d;
+}
+
+__device__ __forceinline__ PixReg reg_pixel_or_empty(const RegParams& p, int x, int y) {
+  if (x >= 0 && x < p.W && y >= 0 && y < p.H) return reg_pixel(p, x, y);
+  PixReg r;
+  r.cover = false; r.n_ok = false; r.zbar = 0.f; r.a_safe = 1e-30f; r.mag = 0.f;
+  for (int i = 0; i < 3; ++i) { r.P[i] = 0.f; r.n[i] = 0.f; }
+  return r;
+}
+
+__device__ __forceinline__ float tgt_diff_norm(const RegParams& p, int x0, int y0, int x1, int y1) {
+  const float* a = p.target + 3 * ((size_t)y0 * p.W + x0);
+  const float* b = p.target + 3 * ((size_t)y1 * p.W + x1);
+  const float d0 = b[0] - a[0], d1 = b[1] - a[1], d2 = b[2] - a[2];
+  return sqrtf(d0 * d0 + d1 * d1 + d2 * d2);
+}
+
+// Smoothness pair term (q, q+e): weight, difference and its norm; valid
+// when both pixels have a covered unit normal.
+struct SmoothPair {
+  bool v;
+  float w, m;
+  float d[3];
+};
+
+__device__ __forceinline__ SmoothPair smooth_pair(const RegParams& p, const PixReg& a,
+                                                  const PixReg& b, int xa, int ya, int xb, int yb) {
+  SmoothPair s;
+  s.v = (a.n_ok && a.cover) && (b.n_ok && b.cover);
+  for (int i = 0; i < 3; ++i) s.d[i] = b.n[i] - a.n[i];
+  s.m = sqrtf(s.d[0] * s.d[0] + s.d[1] * s.d[1] + s.d[2] * s.d[2]);
+  s.w = s.v ? expf(-tgt_diff_norm(p, xa, ya, xb, yb)) : 0.0f;
+  return s;
+}
+
+// Pass A: loss sums and the valid counts.
+__global__ void __launch_bounds__(256) k_reg_count(RegParams p) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  double nsum = 0.0, ncnt = 0.0, ssum = 0.0, scnt = 0.0;
+  if (x < p.W) {
+    const PixReg q = reg_pixel(p, x, y);
+    const bool has_x = x + 1 < p.W, has_y = y + 1 < p.H;
+    const PixReg qx = reg_pixel_or_empty(p, x + 1, y);
+    const PixReg qy = reg_pixel_or_empty(p, x, y + 1);
+    if (p.w_normal > 0.0f) {
+      const DepthNrm d = depth_normal(p, q, qx, qy, has_x && has_y);
+      const bool valid = q.n_ok && d.ok && q.cover;
+      if (valid) {
+        nsum += 1.0 - (double)(q.n[0] * d.n_world[0] + q.n[1] * d.n_world[1] + q.n[2] * d.n_world[2]);
+        ncnt += 1.0;
+      }
+    }
+    if (p.w_smooth > 0.0f) {
+      if (has_x) {
+        const SmoothPair s = smooth_pair(p, q, qx, x, y, x + 1, y);
+        if (s.v) { ssum += (double)(s.w * s.m); scnt += 1.0; }
+      }
+      if (has_y) {
+        const SmoothPair s = smooth_pair(p, q, qy, x, y, x, y + 1);
+        if (s.v) { ssum += (double)(s.w * s.m); scnt += 1.0; }
+      }
+    }
+  }
+  block_sum_atomic(nsum, p.terms + 3);
+  block_sum_atomic(ncnt, p.terms + 4);
+  block_sum_atomic(ssum, p.terms + 5);
+  block_sum_atomic(scnt, p.terms + 6);
+}
+
+// G(q) of depth_to_normal_backward: the oriented view-normal adjoint of the
+// normal-consistency term at q (0 outside [0,W-2] x [0,H-2] or invalid).
+__device__ __forceinline__ void depth_adjoint_at(const RegParams& p, int x, int y, float scale_n,
+                                                 float* G, float* dx, float* dy) {
+  for (int i = 0; i < 3; ++i) { G[i] = 0.f; dx[i] = 0.f; dy[i] = 0.f; }
+  if (x < 0 || y < 0 || x + 1 >= p.W || y + 1 >= p.H) return;
+  const PixReg q = reg_pixel(p, x, y), qx = reg_pixel(p, x + 1, y), qy = reg_pixel(p, x, y + 1);
+  const DepthNrm d = depth_normal(p, q, qx, qy, true);
+  for (int i = 0; i < 3; ++i) { dx[i] = d.dx[i]; dy[i] = d.dy[i]; }
+  const bool valid = q.n_ok && d.ok && q.cover;
+  // upstream on n_ref: w_normal * (-1/n) * n_img; up_v = upstream @ R^T
+  float upv[3];
+  for (int i = 0; i < 3; ++i)
+    upv[i] = -scale_n * (q.n[0] * p.R[i * 3 + 0] + q.n[1] * p.R[i * 3 + 1] + q.n[2] * p.R[i * 3 + 2]);
+  const float dot = d.unit_v[0] * upv[0] + d.unit_v[1] * upv[1] + d.unit_v[2] * upv[2];
+  const float im = 1.0f / fmaxf(d.mag, 1e-30f);
+  for (int i = 0; i < 3; ++i) {
+    const float g = (upv[i] - d.unit_v[i] * dot) * im;
+    G[i] = valid ? (d.flip ? -g : g) : 0.0f;
+  }
+}
+
+// smoothness adjoint of pair (q, q+e): gx = w/m * d / count (0 if m <= 1e-12)
+__device__ __forceinline__ void smooth_adjoint(const RegParams& p, int xa, int ya, int xb, int yb,
+                                               float inv_count, float* g) {
+  g[0] = g[1] = g[2] = 0.f;
+  if (xa < 0 || ya < 0 || xb >= p.W || yb >= p.H) return;
+  const PixReg a = reg_pixel(p, xa, ya), b = reg_pixel(p, xb, yb);
+  const SmoothPair s = smooth_pair(p, a, b, xa, ya, xb, yb);
+  if (!(s.v && s.m > 1e-12f)) return;
+  const float f = s.w / fmaxf(s.m, 1e-30f) * inv_count;
+  for (int i = 0; i < 3; ++i) g[i] = f * s.d[i];
+}
+
+// Pass B: gradients into the G-buffer (normal channels 5..7, depth 11,
+// alpha 12), compute_step's chain (training.py:152-172).
+__global__ void __launch_bounds__(256) k_reg_grad(RegParams p) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= p.W) return;
+  const double ncnt = fmax(p.terms[4], 1.0), scnt = fmax(p.terms[6], 1.0);
+  const float scale_n = (float)(1.0 / ncnt) * p.w_normal;  // w_normal / n
+  const float inv_s = (float)(1.0 / scnt);
+  const size_t HW = (size_t)p.W * p.H, pix = (size_t)y * p.W + x;
+  const PixReg q = reg_pixel(p, x, y);
+  float dn[3] = {0.f, 0.f, 0.f};
+  if (p.w_normal > 0.0f) {
+    // d/dn_img of the consistency term: -(w/n) n_ref on valid pixels
+    if (x + 1 < p.W && y + 1 < p.H) {
+      const PixReg qx = reg_pixel(p, x + 1, y), qy = reg_pixel(p, x, y + 1);
+      const DepthNrm d = depth_normal(p, q, qx, qy, true);
+      if (q.n_ok && d.ok && q.cover)
+        for (int i = 0; i < 3; ++i) dn[i] += -scale_n * d.n_world[i];
+    }
+    // depth adjoint: dpx(p) = ddx(p-x) - ddx(p) + ddy(p-y) - ddy(p)
+    float G[3], dx[3], dy[3], t[3], dpx[3] = {0.f, 0.f, 0.f};
+    depth_adjoint_at(p, x, y, scale_n, G, dx, dy);
+    cross3(dy, G, t);                      // ddx(p)
+    for (int i = 0; i < 3; ++i) dpx[i] -= t[i];
+    cross3(G, dx, t);                      // ddy(p)
+    for (int i = 0; i < 3; ++i) dpx[i] -= t[i];
+    depth_adjoint_at(p, x - 1, y, scale_n, G, dx, dy);
+    cross3(dy, G, t);                      // ddx(p - x)
+    for (int i = 0; i < 3; ++i) dpx[i] += t[i];
+    depth_adjoint_at(p, x, y - 1, scale_n, G, dx, dy);
+    cross3(G, dx, t);                      // ddy(p - y)
+    for (int i = 0; i < 3; ++i) dpx[i] += t[i];
+    const float xs = (float)((((double)x + 0.5) - p.cx) / p.fx);
+    const float ys = (float)((((double)y + 0.5) - p.cy) / p.fy);
+    const float dd = dpx[0] * xs + dpx[1] * ys + dpx[2];
+    if (q.cover) {
+      p.dgbuf[11 * HW + pix] += dd / q.a_safe;
+      p.dgbuf[12 * HW + pix] -= dd * q.zbar / q.a_safe;
+    }
+  }
+  if (p.w_smooth > 0.0f) {
+    float g[3];
+    const float ws = p.w_smooth;
+    smooth_adjoint(p, x - 1, y, x, y, inv_s, g);   // gx(p - x): +
+    for (int i = 0; i < 3; ++i) dn[i] += ws * g[i];
+    smooth_adjoint(p, x, y, x + 1, y, inv_s, g);   // gx(p): -
+    for (int i = 0; i < 3; ++i) dn[i] -= ws * g[i];
+    smooth_adjoint(p, x, y - 1, x, y, inv_s, g);   // gy(p - y): +
+    for (int i = 0; i < 3; ++i) dn[i] += ws * g[i];
+    smooth_adjoint(p, x, y, x, y + 1, inv_s, g);   // gy(p): -
+    for (int i = 0; i < 3; ++i) dn[i] -= ws * g[i];
+  }
+  // _normal_image_backward (training.py:121-126)
+  if (q.n_ok) {
+    const float dot = q.n[0] * dn[0] + q.n[1] * dn[1] + q.n[2] * dn[2];
+    const float im = 1.0f / fmaxf(q.mag, 1e-30f);
+    for (int i = 0; i < 3; ++i) p.dgbuf[(5 + i) * HW + pix] += (dn[i] - q.n[i] * dot) * im;
+  }
+}
+
+// ---- K12 Adam over every parameter group in one launch ---------------------
+struct AdamLaunch {
+  tsb_adam_group g[TSB_ADAM_MAX_GROUPS];
+  int64_t start[TSB_ADAM_MAX_GROUPS + 1];  // prefix of element counts
+  int32_t n;
+  double b1, b2, eps;
+  double bc1, bc2;  // 1 - beta^t
+};
+
+template <typename TP>
+__device__ __forceinline__ void adam_elem(const AdamLaunch& A, const tsb_adam_group& g, int64_t i) {
+  TP* prm = static_cast<TP*>(g.param);
+  TP* m = static_cast<TP*>(g.m);
+  TP* v = static_cast<TP*>(g.v);
+  const TP gr = (TP)g.grad[i];
+  const TP mi = (TP)A.b1 * m[i] + (TP)(1.0 - A.b1) * gr;
+  const TP vi = (TP)A.b2 * v[i] + (TP)(1.0 - A.b2) * gr * gr;
+  m[i] = mi;
+  v[i] = vi;
+  const TP mh = mi / (TP)A.bc1, vh = vi / (TP)A.bc2;
+  TP x = prm[i] - (TP)g.lr * mh / (sqrt(vh) + (TP)A.eps);
+  if (g.clamp == TSB_CLAMP_UNIT) x = x < (TP)0 ? (TP)0 : (x > (TP)1 ? (TP)1 : x);
+  else if (g.clamp == TSB_CLAMP_FLOOR) x = x < (TP)g.floor ? (TP)g.floor : x;
+  prm[i] = x;
+}
+
+__global__ void __launch_bounds__(256) k_adam(AdamLaunch A) {
+  const int64_t total = A.start[A.n];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int k = 0;
+    while (k + 1 < A.n && A.start[k + 1] <= e) ++k;
+    const tsb_adam_group& g = A.g[k];
+    const int64_t i = e - A.start[k];
+    if (g.dtype == TSB_F64) adam_elem<double>(A, g, i);
+    else adam_elem<float>(A, g, i);
+  }
+}
+
+// ---- K13 tangent frames ------------------------------------------------------
+__global__ void k_orthonormalize(int32_t P, double* __restrict__ tu, double* __restrict__ tv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  double u[3], v[3];
+  for (int k = 0; k < 3; ++k) { u[k] = tu[3 * i + k]; v[k] = tv[3 * i + k]; }
+  const double nu = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  for (int k = 0; k < 3; ++k) u[k] /= nu;
+  const double d = u[0] * v[0] + u[1] * v[1] + u[2] * v[2];
+  for (int k = 0; k < 3; ++k) v[k] = v[k] - d * u[k];
+  const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  for (int k = 0; k < 3; ++k) { tu[3 * i + k] = u[k]; tv[3 * i + k] = v[k] / nv; }
+}
+
+bool g_win_ready = false;
+
+cudaError_t ensure_window() {
+  if (g_win_ready) return cudaSuccess;
+  float w[2 * kR + 1];
+  double s = 0.0, wd[2 * kR + 1];
+  for (int i = 0; i <= 2 * kR; ++i) {
+    const double x = (double)(i - kR);
+    wd[i] = std::exp(-0.5 * (x / 1.5) * (x / 1.5));
+    s += wd[i];
+  }
+  for (int i = 0; i <= 2 * kR; ++i) w[i] = (float)(wd[i] / s);
+  cudaError_t e = cudaMemcpyToSymbol(c_win, w, sizeof(w));
+  if (e == cudaSuccess) g_win_ready = true;
+  return e;
+}
+
+}  // namespace
+}  // namespace tsb
+
+using namespace tsb;
+
+extern "C" {
+
+int tsb_loss_scratch_size(int32_t width, int32_t height, uint64_t* bytes) {
+  if (width <= 0 || height <= 0 || !bytes) {
+    set_error("tsb_loss_scratch_size: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  *bytes = (uint64_t)(15 + 9) * width * height * sizeof(float);
+  return TSB_OK;
+}
+
+int tsb_loss_image(const float* color, const float* target, int32_t width, int32_t height,
+                   float dssim_weight, float* dcolor, double* terms, void* scratch,
+                   uint64_t scratch_bytes, void* stream) {
+  if (!color || !target || !dcolor || !terms || !scratch || width <= 0 || height <= 0) {
+    set_error("tsb_loss_image: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  const size_t HW = (size_t)width * height;
+  if (scratch_bytes < (15 + 9) * HW * sizeof(float)) {
+    set_error("tsb_loss_image: scratch too small");
+    return TSB_ERR_CAPACITY;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  TSB_CUDA(ensure_window());
+  float* m5 = static_cast<float*>(scratch);
+  float* part = m5 + 15 * HW;
+  float* hb = m5;  // pass 3 output reuses the moment planes
+  const double N = 3.0 * (double)HW;
+  const dim3 rows((width + 255) / 256, height);
+  k_ssim_pass1<<<rows, 256, 0, st>>>(width, height, color, target, m5, terms);
+  TSB_CHECK_LAUNCH("k_ssim_pass1");
+  k_ssim_pass2<<<rows, 256, 0, st>>>(width, height, m5, part,
+                                     (float)(-0.5 * dssim_weight / N), terms);
+  TSB_CHECK_LAUNCH("k_ssim_pass2");
+  k_ssim_pass3<<<dim3((width + 255) / 256, height, 9), 256, 0, st>>>(width, height, part, hb);
+  TSB_CHECK_LAUNCH("k_ssim_pass3");
+  k_ssim_pass4<<<rows, 256, 0, st>>>(width, height, hb, color, target,
+                                     (float)((1.0 - dssim_weight) / N), dcolor);
+  TSB_CHECK_LAUNCH("k_ssim_pass4");
+  return TSB_OK;
+}
+
+int tsb_loss_regularizers(const float* gbuf, const float* target, const tsb_camera* camera,
+                          float normal_weight, float smooth_weight, float* dgbuf, double* terms,
+                          void* stream) {
+  if (!gbuf || !target || !camera || !dgbuf || !terms || camera->width <= 0 ||
+      camera->height <= 0) {
+    set_error("tsb_loss_regularizers: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  if (!(normal_weight > 0.0f) && !(smooth_weight > 0.0f)) return TSB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  RegParams rp;
+  rp.W = camera->width; rp.H = camera->height;
+  rp.fx = camera->fx; rp.fy = camera->fy; rp.cx = camera->cx; rp.cy = camera->cy;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) rp.R[3 * i + j] = (float)camera->world_to_view[4 * i + j];
+  rp.gbuf = gbuf; rp.target = target; rp.dgbuf = dgbuf; rp.terms = terms;
+  rp.w_normal = normal_weight > 0.0f ? normal_weight : 0.0f;
+  rp.w_smooth = smooth_weight > 0.0f ? smooth_weight : 0.0f;
+  const dim3 rows((rp.W + 255) / 256, rp.H);
+  k_reg_count<<<rows, 256, 0, st>>>(rp);
+  TSB_CHECK_LAUNCH("k_reg_count");
+  k_reg_grad<<<rows, 256, 0, st>>>(rp);
+  TSB_CHECK_LAUNCH("k_reg_grad");
+  return TSB_OK;
+}
+
+int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step, double beta1,
+                  double beta2, double eps, void* stream) {
+  if (!groups || num_groups <= 0 || num_groups > TSB_ADAM_MAX_GROUPS || step <= 0) {
+    set_error("tsb_adam_step: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  AdamLaunch A;
+  A.n = num_groups;
+  A.start[0] = 0;
+  for (int k = 0; k < num_groups; ++k) {
+    const tsb_adam_group& g = groups[k];
+    if (g.count < 0 || (g.count > 0 && (!g.param || !g.grad || !g.m || !g.v)) ||
+        (g.dtype != TSB_F32 && g.dtype != TSB_F64)) {
+      set_error("tsb_adam_step: invalid group");
+      return TSB_ERR_VALUE;
+    }
+    A.g[k] = g;
+    A.start[k + 1] = A.start[k] + g.count;
+  }
+  A.b1 = beta1; A.b2 = beta2; A.eps = eps;
+  A.bc1 = 1.0 - std::pow(beta1, step);
+  A.bc2 = 1.0 - std::pow(beta2, step);
+  const int64_t total = A.start[num_groups];
+  if (total == 0) return TSB_OK;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_adam<<<blocks, 256, 0, (cudaStream_t)stream>>>(A);
+  TSB_CHECK_LAUNCH("k_adam");
+  return TSB_OK;
+}
+
+int tsb_orthonormalize_tangents(int32_t num_splats, double* tangent_u, double* tangent_v,
+                                void* stream) {
+  if (num_splats < 0 || (num_splats > 0 && (!tangent_u || !tangent_v))) {
+    set_error("tsb_orthonormalize_tangents: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  if (num_splats == 0) return TSB_OK;
+  k_orthonormalize<<<(num_splats + 255) / 256, 256, 0, (cudaStream_t)stream>>>(num_splats,
+                                                                             tangent_u, tangent_v);
+  TSB_CHECK_LAUNCH("k_orthonormalize");
+  return TSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+"""Training-step kernels (K10-K13, csrc/tsb_train.cu) against a plain
+PyTorch fp32 reference of the same ops (tests/torch_loss_ref.py, autograd
+adjoints) and against the reference's numpy Adam / Gram-Schmidt.
+
+Tolerances: loss terms 1e-5 relative; gradients max abs error <= 2e-3 of the
+array's max magnitude (fp32 blur sums in a different order than conv2d)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2506_13348_b200 import _lib, render_forward, shade_gbuffer, synth
+from paper_2506_13348_b200.training import (LossWeights, _BUFFERS, image_loss_grad,
+                                            linear_to_display, regularizer_grads)
+
+import golden_io as gio
+import torch_loss_ref as ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _close(name, got, want, rel=2e-3):
+    got = got.detach().double().cpu().numpy()
+    want = want.detach().double().cpu().numpy()
+    scale = max(np.abs(want).max(), 1e-12)
+    err = np.abs(got - want).max()
+    assert err <= rel * scale, (name, err, scale)
+
+
+def _frame(seed=11, size=48):
+    truth = synth.make_gradcheck_scene(seed)
+    cam = synth.camera_ring(1, width=size, height=size)[0]
+    lut = gio.lut()
+    gb = render_forward(truth, cam, "perprim")
+    res = shade_gbuffer(gb, cam, truth.environment, lut, background=truth.background)
+    other = truth.copy()
+    other.texels = np.clip(other.texels * 0.7 + 0.2, 0.0, 1.0).astype(np.float32)
+    tgt = linear_to_display(shade_gbuffer(render_forward(other, cam, "perprim"), cam,
+                                          other.environment, lut,
+                                          background=other.background).color)
+    return cam, gb.planar.contiguous(), res.color.contiguous(), tgt.contiguous()
+
+
+@pytest.mark.parametrize("weights", [LossWeights(), LossWeights(0.5, 0.0, 0.0),
+                                     LossWeights(0.2, 0.3, 0.0), LossWeights(0.2, 0.0, 0.4)])
+def test_loss_kernels_match_torch(weights):
+    cam, planar, color, tgt = _frame()
+    H, W = planar.shape[1:]
+    bufs = dict(_BUFFERS.get(W, H, color.device))
+    terms = torch.zeros(8, dtype=torch.float64, device=color.device)
+    bufs["terms"] = terms
+    dcolor = image_loss_grad(color, tgt, weights, bufs).clone()
+    dg = torch.zeros_like(planar)
+    regularizer_grads(planar, tgt, cam, weights, dg, terms)
+    t = terms.cpu().numpy()
+    N = 3 * W * H
+    rterms, rdcolor, rdg = ref.loss_and_grads(color, planar, tgt, cam, weights)
+    image = (1 - weights.dssim) * t[0] / N + weights.dssim * 0.5 * (1 - t[1] / N)
+    assert abs(image - rterms["image"]) <= 1e-5 * max(1.0, abs(rterms["image"]))
+    if weights.normal > 0:
+        assert abs(t[3] / max(t[4], 1) - rterms["normal"]) <= 1e-5
+    if weights.smooth > 0:
+        assert abs(t[5] / max(t[6], 1) - rterms["smooth"]) <= 1e-5
+    _close("dcolor", dcolor, rdcolor)
+    for c in (5, 6, 7, 11, 12):
+        if rdg[c].abs().max() > 0:
+            _close(f"dgbuf[{c}]", dg[c], rdg[c])
+    for c in (0, 1, 2, 3, 4, 8, 9, 10):
+        assert float(dg[c].abs().max()) == 0.0
+
+
+def _np_adam(p, g, m, v, t, lr, b1=0.9, b2=0.999, eps=1e-8):
+    m = b1 * m + (1 - b1) * g
+    v = b2 * v + (1 - b2) * g * g
+    mh, vh = m / (1 - b1 ** t), v / (1 - b2 ** t)
+    return p - lr * mh / (np.sqrt(vh) + eps), m, v
+
+
+def test_adam_matches_reference_numpy():
+    rng = np.random.default_rng(0)
+    dev = torch.device("cuda")
+    specs = [("f64", np.float64, 1000, _lib.CLAMP_NONE, 0.0, 1e-2),
+             ("f64floor", np.float64, 333, _lib.CLAMP_FLOOR, 0.4, 5e-2),
+             ("f32unit", np.float32, 4097, _lib.CLAMP_UNIT, 0.0, 5e-2)]
+    params, grads, moms, host = [], [], [], []
+    arr = (_lib.AdamGroup_t * len(specs))()
+    for i, (_, dt, n, clamp, floor, lr) in enumerate(specs):
+        p0 = rng.uniform(0.0, 1.0, n).astype(dt)
+        prm = torch.from_numpy(p0.copy()).to(dev)
+        g = torch.zeros(n, dtype=torch.float32, device=dev)
+        m, v = torch.zeros_like(prm), torch.zeros_like(prm)
+        params.append(prm); grads.append(g); moms.append((m, v))
+        host.append([p0.astype(np.float64), np.zeros(n), np.zeros(n)])
+        a = arr[i]
+        a.param, a.grad, a.m, a.v = _lib.ptr(prm), _lib.ptr(g), _lib.ptr(m), _lib.ptr(v)
+        a.count, a.lr, a.floor, a.clamp = n, lr, floor, clamp
+        a.dtype = _lib.F64 if dt == np.float64 else _lib.F32
+    L = _lib.lib()
+    for step in range(1, 4):
+        for i, (_, dt, n, clamp, floor, lr) in enumerate(specs):
+            gh = rng.normal(0.0, 1.0, n).astype(np.float32)
+            grads[i].copy_(torch.from_numpy(gh))
+            p, m, v = _np_adam(host[i][0], gh.astype(np.float64), host[i][1], host[i][2], step, lr)
+            if clamp == _lib.CLAMP_UNIT:
+                p = np.clip(p, 0.0, 1.0)
+            elif clamp == _lib.CLAMP_FLOOR:
+                p = np.maximum(p, floor)
+            host[i] = [p, m, v]
+        _lib.check(L.tsb_adam_step(arr, len(specs), step, 0.9, 0.999, 1e-8, None), "adam")
+        torch.cuda.synchronize()
+        for i, (name, dt, *_r) in enumerate(specs):
+            got = params[i].cpu().numpy().astype(np.float64)
+            tol = 1e-12 if dt == np.float64 else 2e-6
+            assert np.abs(got - host[i][0]).max() <= tol, (name, step)
+
+
+def test_orthonormalize_tangents_matches_reference():
+    rng = np.random.default_rng(1)
+    P = 1000
+    tu = rng.normal(size=(P, 3))
+    tv = rng.normal(size=(P, 3))
+    u = tu / np.linalg.norm(tu, axis=-1, keepdims=True)
+    v = tv - np.sum(u * tv, axis=-1, keepdims=True) * u
+    v = v / np.linalg.norm(v, axis=-1, keepdims=True)
+    du, dv = torch.from_numpy(tu).cuda(), torch.from_numpy(tv).cuda()
+    _lib.check(_lib.lib().tsb_orthonormalize_tangents(P, _lib.ptr(du), _lib.ptr(dv), None), "o")
+    assert np.abs(du.cpu().numpy() - u).max() < 1e-14
+    assert np.abs(dv.cpu().numpy() - v).max() < 1e-14
+
+
+def test_trainer_step_gradient_equals_compute_step():
+    """The trainer's flat buffer (interleaved texel layout, fused packing)
+    holds exactly compute_step's gradients for the same parameters."""
+    from paper_2506_13348_b200.training import DataParallelTrainer, compute_step
+    truth = synth.make_gradcheck_scene(11)
+    cam = synth.camera_ring(1, width=32, height=32)[0]
+    lut = gio.lut()
+    tgt = linear_to_display(shade_gbuffer(render_forward(truth, cam, "perprim"), cam,
+                                          truth.environment, lut,
+                                          background=truth.background).color)
+    init = truth.copy()
+    init.texels = np.clip(init.texels + 0.1, 0.0, 1.0).astype(np.float32)
+    tr = DataParallelTrainer(init, lut)
+    terms = tr.grads_and_loss(cam, tgt)
+    m, grads, eg = compute_step(init, cam, tgt.cpu().numpy(), lut)
+    assert abs(terms["loss"] - m["loss"]) <= 1e-6 * max(1.0, abs(m["loss"]))
+    for name in ("positions", "tangent_u", "tangent_v", "scales", "opacities", "sh"):
+        _close(name, getattr(tr.grads, name), getattr(grads, name), rel=1e-3)
+    got_tex = tr.grads.texels_dense[..., [0, 1, 2, 3, 6, 4, 5]]
+    _close("texels", got_tex, grads.texels_dense, rel=1e-3)
+    for a, b in zip(tr.env_grads.spec_mips, eg.spec_mips):
+        _close("env", a, b, rel=1e-3)
