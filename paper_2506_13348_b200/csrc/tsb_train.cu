@@ -50,11 +50,28 @@ __device__ __forceinline__ float display_slope(float x) {
   return x < 0.0f ? 0.0f : s;
 }
 
-__device__ __forceinline__ void block_sum_atomic(double v, double* dst) {
+// Block-wide sums of K values (blockDim 256), one fp64 atomic per value per
+// block (blocks cover several image rows, so a frame issues a few hundred).
+template <int K>
+__device__ __forceinline__ void block_sums_atomic(double (&v)[K], double* dst) {
+  __shared__ double s_part[8][K];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0 && v != 0.0) atomicAdd(dst, v);
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_part[warp][k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_part[w][threadIdx.x];
+    if (t != 0.0) atomicAdd(dst + threadIdx.x, t);
+  }
 }
+
+constexpr int kRowsPerBlock = 8;
 
 // ---- K10 pass 1: display images, L1 / MSE sums, horizontal blur of the
 // five SSIM moments (a, b, a^2, b^2, ab) per channel -> m5[15][H][W].
@@ -63,43 +80,61 @@ __global__ void __launch_bounds__(256) k_ssim_pass1(int W, int H, const float* _
                                                     float* __restrict__ m5,
                                                     double* __restrict__ terms) {
   __shared__ float sa[3][256 + 2 * kR], sb[3][256 + 2 * kR];
-  const int y = blockIdx.y;
   const int x0 = blockIdx.x * 256;
   const int x = x0 + threadIdx.x;
-  for (int i = threadIdx.x; i < 256 + 2 * kR; i += 256) {
-    const int xx = x0 - kR + i;
-    const bool ok = xx >= 0 && xx < W;
-    for (int c = 0; c < 3; ++c) {
-      const size_t o = 3 * ((size_t)y * W + xx) + c;
-      sa[c][i] = ok ? display_of(color[o]) : 0.0f;
-      sb[c][i] = ok ? target[o] : 0.0f;
-    }
-  }
-  __syncthreads();
-  double l1 = 0.0, se = 0.0;
-  if (x < W) {
-    const size_t HW = (size_t)W * H, pix = (size_t)y * W + x;
-    for (int c = 0; c < 3; ++c) {
-      const float a = sa[c][threadIdx.x + kR], b = sb[c][threadIdx.x + kR];
-      l1 += fabsf(a - b);
-      const float d = fminf(fmaxf(a, 0.f), 1.f) - fminf(fmaxf(b, 0.f), 1.f);
-      se += d * d;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
-#pragma unroll
-      for (int t = 0; t <= 2 * kR; ++t) {
-        const float w = c_win[t], av = sa[c][threadIdx.x + t], bv = sb[c][threadIdx.x + t];
-        s0 += w * av;
-        s1 += w * bv;
-        s2 += w * av * av;
-        s3 += w * bv * bv;
-        s4 += w * av * bv;
+  const size_t HW = (size_t)W * H;
+  double acc[3] = {0.0, 0.0, 0.0};  // L1, (SSIM: pass 2), squared error
+  const int y1 = min(H, (int)(blockIdx.y + 1) * kRowsPerBlock);
+  for (int y = blockIdx.y * kRowsPerBlock; y < y1; ++y) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256 + 2 * kR; i += 256) {
+      const int xx = x0 - kR + i;
+      const bool ok = xx >= 0 && xx < W;
+      for (int c = 0; c < 3; ++c) {
+        const size_t o = 3 * ((size_t)y * W + xx) + c;
+        sa[c][i] = ok ? display_of(color[o]) : 0.0f;
+        sb[c][i] = ok ? target[o] : 0.0f;
       }
-      float* o = m5 + (size_t)(5 * c) * HW + pix;
-      o[0] = s0; o[HW] = s1; o[2 * HW] = s2; o[3 * HW] = s3; o[4 * HW] = s4;
+    }
+    __syncthreads();
+    if (x < W) {
+      const size_t pix = (size_t)y * W + x;
+      for (int c = 0; c < 3; ++c) {
+        const float a = sa[c][threadIdx.x + kR], b = sb[c][threadIdx.x + kR];
+        acc[0] += fabsf(a - b);
+        const float d = fminf(fmaxf(a, 0.f), 1.f) - fminf(fmaxf(b, 0.f), 1.f);
+        acc[2] += d * d;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+#pragma unroll
+        for (int t = 0; t <= 2 * kR; ++t) {
+          const float w = c_win[t], av = sa[c][threadIdx.x + t], bv = sb[c][threadIdx.x + t];
+          s0 += w * av;
+          s1 += w * bv;
+          s2 += w * av * av;
+          s3 += w * bv * bv;
+          s4 += w * av * bv;
+        }
+        float* o = m5 + (size_t)(5 * c) * HW + pix;
+        o[0] = s0; o[HW] = s1; o[2 * HW] = s2; o[3 * HW] = s3; o[4 * HW] = s4;
+      }
     }
   }
-  block_sum_atomic(l1, terms + 0);
-  block_sum_atomic(se, terms + 2);
+  block_sums_atomic(acc, terms);
+}
+
+// Vertical 11-tap blur of NP planes over a TX x TY tile staged in shared
+// memory (rows [y0-5, y0+TY+5) of 32 columns): every input value is read
+// from global once (+ the halo), taps come from conflict-free smem.
+constexpr int kTX = 32, kTY = 48, kTR = kTY + 2 * kR;
+
+template <int NP>
+__device__ __forceinline__ void stage_vtile(float (*tile)[kTR][kTX + 1], const float* __restrict__ src,
+                                            size_t HW, int W, int H, int x0, int y0) {
+  for (int i = threadIdx.x; i < NP * kTR * kTX; i += blockDim.x) {
+    const int pl = i / (kTR * kTX), r = (i / kTX) % kTR, cx = i % kTX;
+    const int yy = y0 - kR + r, xx = x0 + cx;
+    tile[pl][r][cx] = (yy >= 0 && yy < H && xx < W) ? src[pl * HW + (size_t)yy * W + xx] : 0.0f;
+  }
 }
 
 // ---- K10 pass 2: vertical blur of the moments, SSIM map, its sum and the
@@ -108,38 +143,43 @@ __global__ void __launch_bounds__(256) k_ssim_pass1(int W, int H, const float* _
 __global__ void __launch_bounds__(256) k_ssim_pass2(int W, int H, const float* __restrict__ m5,
                                                     float* __restrict__ part, float g,
                                                     double* __restrict__ terms) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-  double msum = 0.0;
-  if (x < W) {
-    const size_t HW = (size_t)W * H, pix = (size_t)y * W + x;
-    for (int c = 0; c < 3; ++c) {
+  __shared__ float tile[5][kTR][kTX + 1];
+  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x = x0 + tx;
+  const size_t HW = (size_t)W * H;
+  double msum[1] = {0.0};
+  for (int c = 0; c < 3; ++c) {
+    __syncthreads();
+    stage_vtile<5>(tile, m5 + (size_t)(5 * c) * HW, HW, W, H, x0, y0);
+    __syncthreads();
+    for (int r = ty; r < kTY; r += 8) {
+      const int y = y0 + r;
+      if (y >= H || x >= W) continue;
       float mom[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int t = 0; t <= 2 * kR; ++t) {
-        const int yy = y - kR + t;
-        if (yy < 0 || yy >= H) continue;
         const float w = c_win[t];
-        const float* src = m5 + (size_t)(5 * c) * HW + (size_t)yy * W + x;
 #pragma unroll
-        for (int k = 0; k < 5; ++k) mom[k] += w * src[k * HW];
+        for (int k = 0; k < 5; ++k) mom[k] += w * tile[k][r + t][tx];
       }
       const float mu_a = mom[0], mu_b = mom[1];
       const float saa = mom[2] - mu_a * mu_a, sbb = mom[3] - mu_b * mu_b;
       const float sab = mom[4] - mu_a * mu_b;
       const float p = 2.0f * mu_a * mu_b + kSsimC1, q = 2.0f * sab + kSsimC2;
-      const float r = mu_a * mu_a + mu_b * mu_b + kSsimC1, s = saa + sbb + kSsimC2;
-      const float m = (p * q) / (r * s);
-      msum += m;
-      const float rs = r * s;
+      const float rr = mu_a * mu_a + mu_b * mu_b + kSsimC1, ss = saa + sbb + kSsimC2;
+      const float m = (p * q) / (rr * ss);
+      msum[0] += m;
+      const float rs = rr * ss;
       const float g_p = g * q / rs, g_q = g * p / rs;
-      const float g_r = -g * m / r, g_s = -g * m / s;
+      const float g_r = -g * m / rr, g_s = -g * m / ss;
       const float g_sab = 2.0f * g_q, g_saa = g_s;
       const float g_mu_a = 2.0f * mu_b * g_p + 2.0f * mu_a * g_r - mu_b * g_sab - 2.0f * mu_a * g_saa;
-      float* o = part + (size_t)(3 * c) * HW + pix;
+      float* o = part + (size_t)(3 * c) * HW + (size_t)y * W + x;
       o[0] = g_mu_a; o[HW] = g_saa; o[2 * HW] = g_sab;
     }
   }
-  block_sum_atomic(msum, terms + 1);
+  block_sums_atomic(msum, terms + 1);
 }
 
 // ---- K10 pass 3: horizontal blur of the 9 adjoint planes.
@@ -169,27 +209,34 @@ __global__ void __launch_bounds__(256) k_ssim_pass4(int W, int H, const float* _
                                                     const float* __restrict__ color,
                                                     const float* __restrict__ target,
                                                     float l1_scale, float* __restrict__ dcolor) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-  if (x >= W) return;
-  const size_t HW = (size_t)W * H, pix = (size_t)y * W + x;
+  __shared__ float tile[3][kTR][kTX + 1];
+  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x = x0 + tx;
+  const size_t HW = (size_t)W * H;
   for (int c = 0; c < 3; ++c) {
-    float v[3] = {0.f, 0.f, 0.f};
+    __syncthreads();
+    stage_vtile<3>(tile, hb + (size_t)(3 * c) * HW, HW, W, H, x0, y0);
+    __syncthreads();
+    for (int r = ty; r < kTY; r += 8) {
+      const int y = y0 + r;
+      if (y >= H || x >= W) continue;
+      float v[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-    for (int t = 0; t <= 2 * kR; ++t) {
-      const int yy = y - kR + t;
-      if (yy < 0 || yy >= H) continue;
-      const float w = c_win[t];
-      const float* src = hb + (size_t)(3 * c) * HW + (size_t)yy * W + x;
-      v[0] += w * src[0];
-      v[1] += w * src[HW];
-      v[2] += w * src[2 * HW];
+      for (int t = 0; t <= 2 * kR; ++t) {
+        const float w = c_win[t];
+        v[0] += w * tile[0][r + t][tx];
+        v[1] += w * tile[1][r + t][tx];
+        v[2] += w * tile[2][r + t][tx];
+      }
+      const size_t pix = (size_t)y * W + x;
+      const float cx = color[3 * pix + c];
+      const float a = display_of(cx), b = target[3 * pix + c];
+      const float d = a - b;
+      const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+      const float dpred = l1_scale * sg + v[0] + 2.0f * a * v[1] + b * v[2];
+      dcolor[3 * pix + c] = dpred * display_slope(cx);
     }
-    const float cx = color[3 * pix + c];
-    const float a = display_of(cx), b = target[3 * pix + c];
-    const float d = a - b;
-    const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-    const float dpred = l1_scale * sg + v[0] + 2.0f * a * v[1] + b * v[2];
-    dcolor[3 * pix + c] = dpred * display_slope(cx);
   }
 }
 
@@ -314,9 +361,10 @@ __device__ __forceinline__ SmoothPair smooth_pair(const RegParams& p, const PixR
 
 // Pass A: loss sums and the valid counts.
 __global__ void __launch_bounds__(256) k_reg_count(RegParams p) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-  double nsum = 0.0, ncnt = 0.0, ssum = 0.0, scnt = 0.0;
-  if (x < p.W) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // normal sum, normal count, smooth sum, smooth count
+  const int y1 = min(p.H, (int)(blockIdx.y + 1) * kRowsPerBlock);
+  for (int y = blockIdx.y * kRowsPerBlock; y < y1 && x < p.W; ++y) {
     const PixReg q = reg_pixel(p, x, y);
     const bool has_x = x + 1 < p.W, has_y = y + 1 < p.H;
     const PixReg qx = reg_pixel_or_empty(p, x + 1, y);
@@ -325,25 +373,22 @@ __global__ void __launch_bounds__(256) k_reg_count(RegParams p) {
       const DepthNrm d = depth_normal(p, q, qx, qy, has_x && has_y);
       const bool valid = q.n_ok && d.ok && q.cover;
       if (valid) {
-        nsum += 1.0 - (double)(q.n[0] * d.n_world[0] + q.n[1] * d.n_world[1] + q.n[2] * d.n_world[2]);
-        ncnt += 1.0;
+        acc[0] += 1.0 - (double)(q.n[0] * d.n_world[0] + q.n[1] * d.n_world[1] + q.n[2] * d.n_world[2]);
+        acc[1] += 1.0;
       }
     }
     if (p.w_smooth > 0.0f) {
       if (has_x) {
         const SmoothPair s = smooth_pair(p, q, qx, x, y, x + 1, y);
-        if (s.v) { ssum += (double)(s.w * s.m); scnt += 1.0; }
+        if (s.v) { acc[2] += (double)(s.w * s.m); acc[3] += 1.0; }
       }
       if (has_y) {
         const SmoothPair s = smooth_pair(p, q, qy, x, y, x, y + 1);
-        if (s.v) { ssum += (double)(s.w * s.m); scnt += 1.0; }
+        if (s.v) { acc[2] += (double)(s.w * s.m); acc[3] += 1.0; }
       }
     }
   }
-  block_sum_atomic(nsum, p.terms + 3);
-  block_sum_atomic(ncnt, p.terms + 4);
-  block_sum_atomic(ssum, p.terms + 5);
-  block_sum_atomic(scnt, p.terms + 6);
+  block_sums_atomic(acc, p.terms + 3);
 }
 
 // G(q) of depth_to_normal_backward: the oriented view-normal adjoint of the
@@ -441,41 +486,92 @@ __global__ void __launch_bounds__(256) k_reg_grad(RegParams p) {
 }
 
 // ---- K12 Adam over every parameter group in one launch ---------------------
+constexpr int kAdamChunk = 256 * 8;  // elements per block
+
 struct AdamLaunch {
   tsb_adam_group g[TSB_ADAM_MAX_GROUPS];
-  int64_t start[TSB_ADAM_MAX_GROUPS + 1];  // prefix of element counts
+  int32_t blk_start[TSB_ADAM_MAX_GROUPS + 1];  // first block of each group
   int32_t n;
   double b1, b2, eps;
   double bc1, bc2;  // 1 - beta^t
 };
 
 template <typename TP>
-__device__ __forceinline__ void adam_elem(const AdamLaunch& A, const tsb_adam_group& g, int64_t i) {
+__device__ __forceinline__ void adam_chunk(const AdamLaunch& A, const tsb_adam_group& g,
+                                           int64_t base) {
   TP* prm = static_cast<TP*>(g.param);
   TP* m = static_cast<TP*>(g.m);
   TP* v = static_cast<TP*>(g.v);
-  const TP gr = (TP)g.grad[i];
-  const TP mi = (TP)A.b1 * m[i] + (TP)(1.0 - A.b1) * gr;
-  const TP vi = (TP)A.b2 * v[i] + (TP)(1.0 - A.b2) * gr * gr;
-  m[i] = mi;
-  v[i] = vi;
-  const TP mh = mi / (TP)A.bc1, vh = vi / (TP)A.bc2;
-  TP x = prm[i] - (TP)g.lr * mh / (sqrt(vh) + (TP)A.eps);
-  if (g.clamp == TSB_CLAMP_UNIT) x = x < (TP)0 ? (TP)0 : (x > (TP)1 ? (TP)1 : x);
-  else if (g.clamp == TSB_CLAMP_FLOOR) x = x < (TP)g.floor ? (TP)g.floor : x;
-  prm[i] = x;
+  const TP b1 = (TP)A.b1, b2 = (TP)A.b2, c1 = (TP)(1.0 - A.b1), c2 = (TP)(1.0 - A.b2);
+  const TP ibc1 = (TP)(1.0 / A.bc1), ibc2 = (TP)(1.0 / A.bc2), lr = (TP)g.lr, eps = (TP)A.eps;
+#pragma unroll 4
+  for (int j = 0; j < kAdamChunk / 256; ++j) {
+    const int64_t i = base + j * 256 + threadIdx.x;
+    if (i >= g.count) break;
+    const TP gr = (TP)__ldg(g.grad + i);
+    const TP mi = b1 * m[i] + c1 * gr;
+    const TP vi = b2 * v[i] + c2 * gr * gr;
+    m[i] = mi;
+    v[i] = vi;
+    TP x = prm[i] - lr * (mi * ibc1) / (sqrt(vi * ibc2) + eps);
+    if (g.clamp == TSB_CLAMP_UNIT) x = x < (TP)0 ? (TP)0 : (x > (TP)1 ? (TP)1 : x);
+    else if (g.clamp == TSB_CLAMP_FLOOR) x = x < (TP)g.floor ? (TP)g.floor : x;
+    prm[i] = x;
+  }
 }
 
+__device__ __forceinline__ float adam_f(float p, float gr, float& m, float& v, float b1, float b2,
+                                        float c1, float c2, float ibc1, float ibc2, float lr,
+                                        float eps, const tsb_adam_group& g) {
+  m = b1 * m + c1 * gr;
+  v = b2 * v + c2 * gr * gr;
+  float x = p - lr * (m * ibc1) / (sqrtf(v * ibc2) + eps);
+  if (g.clamp == TSB_CLAMP_UNIT) x = fminf(fmaxf(x, 0.f), 1.f);
+  else if (g.clamp == TSB_CLAMP_FLOOR) x = fmaxf(x, (float)g.floor);
+  return x;
+}
+
+// float32 groups with 16-B aligned, multiple-of-4 arrays: 128-bit accesses
+__device__ __forceinline__ void adam_chunk_f4(const AdamLaunch& A, const tsb_adam_group& g,
+                                              int64_t base) {
+  float4* prm = static_cast<float4*>(g.param);
+  float4* m4 = static_cast<float4*>(g.m);
+  float4* v4 = static_cast<float4*>(g.v);
+  const float4* g4 = reinterpret_cast<const float4*>(g.grad);
+  const float b1 = (float)A.b1, b2 = (float)A.b2, c1 = (float)(1.0 - A.b1), c2 = (float)(1.0 - A.b2);
+  const float ibc1 = (float)(1.0 / A.bc1), ibc2 = (float)(1.0 / A.bc2), lr = (float)g.lr;
+  const float eps = (float)A.eps;
+  const int64_t n4 = g.count / 4;
+#pragma unroll 2
+  for (int j = 0; j < kAdamChunk / 1024; ++j) {
+    const int64_t i = base / 4 + j * 256 + threadIdx.x;
+    if (i >= n4) break;
+    const float4 gr = __ldg(g4 + i);
+    float4 p = prm[i], m = m4[i], v = v4[i];
+    p.x = adam_f(p.x, gr.x, m.x, v.x, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+    p.y = adam_f(p.y, gr.y, m.y, v.y, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+    p.z = adam_f(p.z, gr.z, m.z, v.z, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+    p.w = adam_f(p.w, gr.w, m.w, v.w, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+    prm[i] = p; m4[i] = m; v4[i] = v;
+  }
+}
+
+// One block = one contiguous chunk of one group (coalesced, no per-element
+// group search).
 __global__ void __launch_bounds__(256) k_adam(AdamLaunch A) {
-  const int64_t total = A.start[A.n];
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int k = 0;
-    while (k + 1 < A.n && A.start[k + 1] <= e) ++k;
-    const tsb_adam_group& g = A.g[k];
-    const int64_t i = e - A.start[k];
-    if (g.dtype == TSB_F64) adam_elem<double>(A, g, i);
-    else adam_elem<float>(A, g, i);
+  int k = 0;
+  while (k + 1 < A.n && A.blk_start[k + 1] <= (int)blockIdx.x) ++k;
+  const tsb_adam_group& g = A.g[k];
+  const int64_t base = (int64_t)(blockIdx.x - A.blk_start[k]) * kAdamChunk;
+  if (g.dtype == TSB_F64) {
+    adam_chunk<double>(A, g, base);
+  } else if ((g.count & 3) == 0 && ((reinterpret_cast<uintptr_t>(g.param) |
+                                     reinterpret_cast<uintptr_t>(g.m) |
+                                     reinterpret_cast<uintptr_t>(g.v) |
+                                     reinterpret_cast<uintptr_t>(g.grad)) & 15) == 0) {
+    adam_chunk_f4(A, g, base);
+  } else {
+    adam_chunk<float>(A, g, base);
   }
 }
 
@@ -545,14 +641,16 @@ int tsb_loss_image(const float* color, const float* target, int32_t width, int32
   float* hb = m5;  // pass 3 output reuses the moment planes
   const double N = 3.0 * (double)HW;
   const dim3 rows((width + 255) / 256, height);
-  k_ssim_pass1<<<rows, 256, 0, st>>>(width, height, color, target, m5, terms);
+  const dim3 strips((width + 255) / 256, (height + kRowsPerBlock - 1) / kRowsPerBlock);
+  k_ssim_pass1<<<strips, 256, 0, st>>>(width, height, color, target, m5, terms);
   TSB_CHECK_LAUNCH("k_ssim_pass1");
-  k_ssim_pass2<<<rows, 256, 0, st>>>(width, height, m5, part,
+  const dim3 vtiles((width + kTX - 1) / kTX, (height + kTY - 1) / kTY);
+  k_ssim_pass2<<<vtiles, 256, 0, st>>>(width, height, m5, part,
                                      (float)(-0.5 * dssim_weight / N), terms);
   TSB_CHECK_LAUNCH("k_ssim_pass2");
   k_ssim_pass3<<<dim3((width + 255) / 256, height, 9), 256, 0, st>>>(width, height, part, hb);
   TSB_CHECK_LAUNCH("k_ssim_pass3");
-  k_ssim_pass4<<<rows, 256, 0, st>>>(width, height, hb, color, target,
+  k_ssim_pass4<<<vtiles, 256, 0, st>>>(width, height, hb, color, target,
                                      (float)((1.0 - dssim_weight) / N), dcolor);
   TSB_CHECK_LAUNCH("k_ssim_pass4");
   return TSB_OK;
@@ -577,7 +675,7 @@ int tsb_loss_regularizers(const float* gbuf, const float* target, const tsb_came
   rp.w_normal = normal_weight > 0.0f ? normal_weight : 0.0f;
   rp.w_smooth = smooth_weight > 0.0f ? smooth_weight : 0.0f;
   const dim3 rows((rp.W + 255) / 256, rp.H);
-  k_reg_count<<<rows, 256, 0, st>>>(rp);
+  k_reg_count<<<dim3(rows.x, (rp.H + kRowsPerBlock - 1) / kRowsPerBlock), 256, 0, st>>>(rp);
   TSB_CHECK_LAUNCH("k_reg_count");
   k_reg_grad<<<rows, 256, 0, st>>>(rp);
   TSB_CHECK_LAUNCH("k_reg_grad");
@@ -592,7 +690,7 @@ int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step
   }
   AdamLaunch A;
   A.n = num_groups;
-  A.start[0] = 0;
+  A.blk_start[0] = 0;
   for (int k = 0; k < num_groups; ++k) {
     const tsb_adam_group& g = groups[k];
     if (g.count < 0 || (g.count > 0 && (!g.param || !g.grad || !g.m || !g.v)) ||
@@ -601,14 +699,18 @@ int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step
       return TSB_ERR_VALUE;
     }
     A.g[k] = g;
-    A.start[k + 1] = A.start[k] + g.count;
+    const int64_t nb = (g.count + kAdamChunk - 1) / kAdamChunk;
+    if ((int64_t)A.blk_start[k] + nb > 0x7fffffff) {
+      set_error("tsb_adam_step: too many elements");
+      return TSB_ERR_VALUE;
+    }
+    A.blk_start[k + 1] = A.blk_start[k] + (int32_t)nb;
   }
   A.b1 = beta1; A.b2 = beta2; A.eps = eps;
   A.bc1 = 1.0 - std::pow(beta1, step);
   A.bc2 = 1.0 - std::pow(beta2, step);
-  const int64_t total = A.start[num_groups];
-  if (total == 0) return TSB_OK;
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  const int blocks = A.blk_start[num_groups];
+  if (blocks == 0) return TSB_OK;
   k_adam<<<blocks, 256, 0, (cudaStream_t)stream>>>(A);
   TSB_CHECK_LAUNCH("k_adam");
   return TSB_OK;
