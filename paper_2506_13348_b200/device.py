@@ -248,10 +248,14 @@ class FrameWorkspace:
         self.buf = None
         self.nbytes = 0
         self.needed = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.shrink_to = None
 
-    def ensure(self, P, W, H, tile, capacity):
+    def ensure(self, P, W, H, tile, capacity, exact: bool = False):
+        """Make room for `capacity` entries. The binning sorts the whole
+        capacity (padding included), so `exact=True` also shrinks."""
         key = (P, W, H, tile)
-        if self.key == key and self.capacity >= capacity:
+        if self.key == key and (self.capacity == capacity or
+                                (not exact and self.capacity >= capacity)):
             return
         cap = max(int(capacity), 1)
         nb = C.c_uint64()

@@ -207,6 +207,9 @@ def render_prepared(prep: PreparedScene, camera, tile: int = TILE, *, out=None,
     ws = prep.workspace
     if ws.key != (P, W, H, tile):
         ws.ensure(P, W, H, tile, FrameWorkspace.initial_capacity(P, W, H, tile))
+    elif getattr(ws, "shrink_to", None):
+        ws.ensure(P, W, H, tile, ws.shrink_to, exact=True)
+        ws.shrink_to = None
     gbuf = out if out is not None else torch.empty((NUM_CHANNELS, H, W), dtype=torch.float32,
                                                    device=dev)
     px = pixels if pixels is not None else PixelState.empty(H, W, dev)
@@ -225,6 +228,10 @@ def render_prepared(prep: PreparedScene, camera, tile: int = TILE, *, out=None,
             break
         needed = int(ws.needed.item())
         if needed <= ws.capacity:
+            # the binning sorts the whole capacity: shrink a generous first
+            # guess for the next frames (this frame's tape keeps its buffer)
+            if ws.capacity > 2 * needed + 65536:
+                ws.shrink_to = int(needed * 1.25) + 4096
             break
         ws.ensure(P, W, H, tile, int(needed * 1.25) + 1024)
     tape = Tape(prep, camera, tile, ws.capacity, ws.buf, ws.nbytes, px, gbuf, mode)

@@ -61,7 +61,8 @@ class Renderer:
         """Pre-size the frame workspace (no per-frame capacity sync needed)."""
         ws = self.prep.workspace
         ws.ensure(self.prep.scene.num_splats, int(camera.width), int(camera.height), self.tile,
-                  entries)
+                  entries, exact=True)
+        ws.shrink_to = None
 
     def entries_needed(self) -> int:
         return int(self.prep.workspace.needed.item())
