@@ -140,7 +140,10 @@ struct PrepParams {
   int32_t* tile_count;
 };
 
-__global__ void __launch_bounds__(256) k_preprocess(PrepParams p) {
+#ifndef TSB_PREP_MINB
+#define TSB_PREP_MINB 3  // 80 registers: 3 CTAs/SM hide the fp64 and store latency
+#endif
+__global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p) {
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= p.P) return;
   const int K = (p.sh_degree + 1) * (p.sh_degree + 1);
