@@ -140,6 +140,25 @@ int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera,
                          int64_t max_entries, float* gbuf,
                          const tsb_pixel_state* pixels, void* stream);
 
+/* Frame graph: tsb_render_forward (+ tsb_shade_forward when env is not
+ * NULL) of one view captured once as a CUDA graph over fixed buffers; each
+ * tsb_frame_graph_launch rewrites only the camera-dependent kernel
+ * parameters (and optionally the colour output) and replays the graph —
+ * the multi-view serving path (cli.py:63-68 per-view body) without ~20
+ * host launches per view. The camera size must match the captured one.
+ * create renders (and shades) the given view once, uncaptured, to validate
+ * the arguments. */
+typedef struct tsb_frame_graph* tsb_frame_graph_t;
+int tsb_frame_graph_create(const tsb_scene* scene, const tsb_camera* camera,
+                           const tsb_atlas* atlas, int32_t mode, int32_t tile,
+                           void* workspace, uint64_t workspace_bytes, int64_t max_entries,
+                           float* gbuf, const tsb_pixel_state* pixels, int64_t* entries_needed,
+                           const tsb_environment* env, const float* background, float* color,
+                           float* diffuse, float* specular, tsb_frame_graph_t* graph);
+int tsb_frame_graph_launch(tsb_frame_graph_t graph, const tsb_camera* camera, float* color,
+                           void* stream);
+int tsb_frame_graph_destroy(tsb_frame_graph_t graph);
+
 /* Copy the frame's structural results out of the workspace (debug/parity):
  * sorted_ids (P, kept splats in draw order then culled ids), keys
  * (max_entries: (tile << 32) | depth_rank of every sorted entry, padding

@@ -119,6 +119,12 @@ _SIGNATURES = {
     "tsb_adam_step": [C.POINTER(AdamGroup_t), C.c_int32, C.c_int32, C.c_double, C.c_double,
                       C.c_double, _P],
     "tsb_orthonormalize_tangents": [C.c_int32, _P, _P, _P],
+    "tsb_frame_graph_create": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
+                               C.c_int32, C.c_int32, _P, C.c_uint64, C.c_int64, _P,
+                               C.POINTER(PixelState_t), _P, C.POINTER(Environment_t), _P, _P,
+                               _P, _P, C.POINTER(C.c_void_p)],
+    "tsb_frame_graph_launch": [_P, C.POINTER(Camera_t), _P, _P],
+    "tsb_frame_graph_destroy": [_P],
 }
 
 _lib = None

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <vector>
 
 #include "tsb_internal.cuh"
 
@@ -1135,6 +1136,180 @@ int tsb_tex_probe(tsb_atlas_tex_t h, int32_t window, int32_t iters, float* sink,
   AtlasTex* t = reinterpret_cast<AtlasTex*>(h);
   k_tex_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(t->tex_a, window, iters, sink);
   TSB_CHECK_LAUNCH("k_tex_probe");
+  return TSB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Frame graph: K1-K6 of one view captured once as a CUDA graph; per view only
+// the camera-dependent kernel parameters (K1, K5, K6) are rewritten and the
+// graph is replayed — one host call instead of ~20 launches.
+// ---------------------------------------------------------------------------
+namespace tsb {
+namespace {
+
+template <int TILE>
+const void* raster_fn_tile(int mode) {
+  if (mode == TSB_MODE_HW) return reinterpret_cast<const void*>(k_raster_fwd<TILE, TSB_MODE_HW>);
+  if (mode == TSB_MODE_VERIFY)
+    return reinterpret_cast<const void*>(k_raster_fwd<TILE, TSB_MODE_VERIFY>);
+  return reinterpret_cast<const void*>(k_raster_fwd<TILE, TSB_MODE_FLAT>);
+}
+
+const void* raster_fn(int tile, int mode) {
+  if (tile == 8) return raster_fn_tile<8>(mode);
+  if (tile == 16) return raster_fn_tile<16>(mode);
+  return raster_fn_tile<32>(mode);
+}
+
+}  // namespace
+}  // namespace tsb
+
+struct tsb_frame_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int32_t width = 0, height = 0;
+  cudaGraphNode_t n_prep = nullptr, n_raster = nullptr, n_shade = nullptr;
+  tsb::PrepParams prep;
+  tsb::RasterParams raster;
+  tsb::ShadeParams shade;
+  cudaKernelNodeParams kp_prep, kp_raster, kp_shade;
+};
+
+extern "C" {
+
+int tsb_frame_graph_destroy(tsb_frame_graph_t g) {
+  if (!g) return TSB_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return TSB_OK;
+}
+
+int tsb_frame_graph_create(const tsb_scene* scene, const tsb_camera* camera, const tsb_atlas* atlas,
+                           int32_t mode, int32_t tile, void* ws, uint64_t ws_bytes, int64_t cap,
+                           float* gbuf, const tsb_pixel_state* px, int64_t* entries_needed,
+                           const tsb_environment* env, const float* background, float* color,
+                           float* diffuse, float* specular, tsb_frame_graph_t* out) {
+  if (!out || !camera) {
+    set_error("tsb_frame_graph_create: null argument");
+    return TSB_ERR_VALUE;
+  }
+  *out = nullptr;
+  if (env && !color) {
+    set_error("tsb_frame_graph_create: shading needs a colour buffer");
+    return TSB_ERR_VALUE;
+  }
+  // one uncaptured frame first: validates the arguments and performs the
+  // one-time attribute / occupancy queries outside the capture
+  int rc = tsb_render_forward(scene, camera, atlas, mode, tile, ws, ws_bytes, cap, gbuf, px,
+                              entries_needed, nullptr);
+  if (rc != TSB_OK) return rc;
+  if (env) {
+    rc = tsb_shade_forward(gbuf, camera, env, background, color, diffuse, specular, nullptr);
+    if (rc != TSB_OK) return rc;
+  }
+  TSB_CUDA(cudaDeviceSynchronize());
+  tsb_frame_graph* g = new tsb_frame_graph();
+  g->width = camera->width;
+  g->height = camera->height;
+  cudaStream_t s;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete g; return cuda_fail("cudaStreamCreate", e); }
+  e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    rc = tsb_render_forward(scene, camera, atlas, mode, tile, ws, ws_bytes, cap, gbuf, px,
+                            entries_needed, s);
+    if (rc == TSB_OK && env)
+      rc = tsb_shade_forward(gbuf, camera, env, background, color, diffuse, specular, s);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+    g->graph = graph;
+    if (rc == TSB_OK && e2 != cudaSuccess) rc = cuda_fail("cudaStreamEndCapture", e2);
+  } else {
+    rc = cuda_fail("cudaStreamBeginCapture", e);
+  }
+  cudaStreamDestroy(s);
+  if (rc != TSB_OK) { tsb_frame_graph_destroy(g); return rc; }
+  // locate the camera-dependent kernel nodes
+  size_t n = 0;
+  TSB_CUDA(cudaGraphGetNodes(g->graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  TSB_CUDA(cudaGraphGetNodes(g->graph, nodes.data(), &n));
+  const void* f_raster = raster_fn(tile, mode);
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    TSB_CUDA(cudaGraphNodeGetType(nd, &t));
+    if (t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp;
+    TSB_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+    if (kp.func == reinterpret_cast<void*>(k_preprocess)) {
+      g->n_prep = nd; g->kp_prep = kp;
+      g->prep = *static_cast<PrepParams*>(kp.kernelParams[0]);
+    } else if (kp.func == f_raster) {
+      g->n_raster = nd; g->kp_raster = kp;
+      g->raster = *static_cast<RasterParams*>(kp.kernelParams[0]);
+    } else if (kp.func == reinterpret_cast<void*>(k_shade)) {
+      g->n_shade = nd; g->kp_shade = kp;
+      g->shade = *static_cast<ShadeParams*>(kp.kernelParams[0]);
+    }
+  }
+  const bool has_splats = scene && scene->num_splats > 0;
+  if ((has_splats && !g->n_prep) || !g->n_raster || (env && !g->n_shade)) {
+    tsb_frame_graph_destroy(g);
+    set_error("tsb_frame_graph_create: kernel nodes not found in the capture");
+    return TSB_ERR_CUDA;
+  }
+  e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (e != cudaSuccess) { tsb_frame_graph_destroy(g); return cuda_fail("cudaGraphInstantiate", e); }
+  *out = g;
+  return TSB_OK;
+}
+
+int tsb_frame_graph_launch(tsb_frame_graph_t g, const tsb_camera* camera, float* color,
+                           void* stream) {
+  if (!g || !camera) {
+    set_error("tsb_frame_graph_launch: null argument");
+    return TSB_ERR_VALUE;
+  }
+  if (camera->width != g->width || camera->height != g->height) {
+    set_error("tsb_frame_graph_launch: camera size differs from the captured frame");
+    return TSB_ERR_VALUE;
+  }
+  if (!(camera->near_z > 0.0) || !(camera->fx > 0.0) || !(camera->fy > 0.0)) {
+    set_error("tsb_frame_graph_launch: invalid camera");
+    return TSB_ERR_VALUE;
+  }
+  const tsb_cam_params cam = to_cam(camera);
+  if (g->n_prep) {
+    g->prep.cam = cam;
+    g->prep.near_bits = tsb_f64_bits(camera->near_z);
+    void* args[] = {&g->prep};
+    cudaKernelNodeParams kp = g->kp_prep;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    TSB_CUDA(cudaGraphExecKernelNodeSetParams(g->exec, g->n_prep, &kp));
+  }
+  {
+    g->raster.cam = cam;
+    g->raster.near_f = (float)camera->near_z;
+    void* args[] = {&g->raster};
+    cudaKernelNodeParams kp = g->kp_raster;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    TSB_CUDA(cudaGraphExecKernelNodeSetParams(g->exec, g->n_raster, &kp));
+  }
+  if (g->n_shade) {
+    g->shade.cam = cam;
+    if (color) g->shade.color = color;
+    void* args[] = {&g->shade};
+    cudaKernelNodeParams kp = g->kp_shade;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    TSB_CUDA(cudaGraphExecKernelNodeSetParams(g->exec, g->n_shade, &kp));
+  }
+  TSB_CUDA(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
   return TSB_OK;
 }
 

@@ -9,8 +9,12 @@ host synchronisation, so a view batch (cfg3) streams back to back.
 
 from __future__ import annotations
 
+import ctypes as C
+
+import numpy as np
 import torch
 
+from . import _lib
 from .device import DeviceAtlas, DeviceEnvironment, DeviceScene, FrameWorkspace
 from .rasterize import NUM_CHANNELS, TILE, GBuffer, PixelState, PreparedScene, prepare, render_prepared
 from .shading import ShadeResult, shade_planar
@@ -39,6 +43,8 @@ class Renderer:
         self.background = background if background is not None else getattr(
             scene, "background", None)
         self._bufs = {}
+        self._graphs = {}           # (W, H) -> (key, handle)
+        self.use_graph = True
 
     @property
     def device(self):
@@ -67,12 +73,64 @@ class Renderer:
     def entries_needed(self) -> int:
         return int(self.prep.workspace.needed.item())
 
+    def _graph(self, camera, W, H):
+        """CUDA graph of this view size over the current buffers (rebuilt if
+        the workspace was reallocated)."""
+        ws = self.prep.workspace
+        gb, px, col, _, _ = self._buffers(W, H)
+        key = (_lib.ptr(ws.buf), ws.capacity, ws.nbytes)
+        cur = self._graphs.get((W, H))
+        if cur is not None and cur[0] == key:
+            return cur[1], col
+        if cur is not None:
+            _lib.lib().tsb_frame_graph_destroy(cur[1])
+            del self._graphs[(W, H)]
+        L = _lib.lib()
+        sc, at, cam = self.prep.scene.struct(), self.prep.atlas.struct(), _lib.camera_struct(camera)
+        pst = px.struct()
+        env = self.env.struct()
+        bg = (C.c_float * 3)(*([0.0] * 3 if self.background is None else
+                               [float(v) for v in np.asarray(self.background, np.float64)]))
+        from .rasterize import _MODES
+        h = C.c_void_p()
+        _lib.check(L.tsb_frame_graph_create(
+            C.byref(sc), C.byref(cam), C.byref(at), _MODES[self.prep.sampler], self.tile,
+            _lib.ptr(ws.buf), ws.nbytes, ws.capacity, _lib.ptr(gb), C.byref(pst),
+            _lib.ptr(ws.needed), C.byref(env), bg, _lib.ptr(col), None, None, C.byref(h)),
+            "tsb_frame_graph_create")
+        self._graphs[(W, H)] = (key, h)
+        return h, col
+
+    def close(self):
+        for _, h in self._graphs.values():
+            _lib.lib().tsb_frame_graph_destroy(h)
+        self._graphs = {}
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 — interpreter shutdown
+            pass
+
     def render(self, camera, *, check: bool = True, want_split: bool = False, stream=None,
                color=None):
         """Forward + shade one view. Returns (color (H,W,3), GBuffer), both on
         the GPU; buffers are reused across calls of the same size (pass
-        `color` to shade into a caller-owned buffer instead)."""
+        `color` to shade into a caller-owned buffer instead). With
+        check=False (workspace already reserved) the view replays a CUDA
+        graph of the whole frame (tsb_frame_graph_*)."""
         W, H = int(camera.width), int(camera.height)
+        ws = self.prep.workspace
+        if (not check and not want_split and self.use_graph and ws.buf is not None
+                and ws.key == (self.prep.scene.num_splats, W, H, self.tile)):
+            h, col = self._graph(camera, W, H)
+            out = color if color is not None else col
+            cam = _lib.camera_struct(camera)
+            _lib.check(_lib.lib().tsb_frame_graph_launch(h, C.byref(cam), _lib.ptr(out),
+                                                         _lib.stream_handle(stream)),
+                       "tsb_frame_graph_launch")
+            gb, px = self._buffers(W, H)[:2]
+            return out, GBuffer(gb, px)
         gb, px, col, dif, spe = self._buffers(W, H)
         if color is not None:
             col = color
@@ -94,11 +152,15 @@ class Renderer:
             return
         W, H = int(cams[0].width), int(cams[0].height)
         dev = self.device
-        dcol = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)]
-        hcol = host_out or [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True)
-                            for _ in range(2)]
+        key = ("stream", W, H)
+        if key not in self._bufs:  # pinned buffers, copy stream: allocated once
+            self._bufs[key] = (
+                [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)],
+                [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True) for _ in range(2)],
+                torch.cuda.Stream(dev))
+        dcol, hcol_cached, copy = self._bufs[key]
+        hcol = host_out or hcol_cached
         compute = torch.cuda.current_stream(dev)
-        copy = torch.cuda.Stream(dev)
         done = [torch.cuda.Event(), torch.cuda.Event()]
         ready = [torch.cuda.Event(), torch.cuda.Event()]
         for i, cam in enumerate(cams):
