@@ -304,3 +304,31 @@ def test_hw_rgba16f_and_multipage_hw_match_counts():
                             texel_format=fmt)                 # 3 pages, layered texture
         assert np.array_equal(_np(gb.pixels.n_contrib), ref["n_contrib"])
         assert psnr(_np(gb.planar)[:12], ref["gbuf"][:12]) >= 50.0
+
+
+def test_frame_graph_matches_launches_and_rejects_other_sizes():
+    """tsb_frame_graph_*: replaying the captured frame for new cameras gives
+    bit-identical colour and G-buffers to the per-launch path."""
+    from paper_2506_13348_b200 import Renderer, pack_atlases
+    from paper_2506_13348_b200.environment import BrdfLut
+    scene = synth.make_shell_scene(3000, 4, seed=3, with_environment=True, env_height=16,
+                                   env_levels=3)
+    cams = synth.bench_cameras(5, 96, 80)
+    r = Renderer(scene, pack_atlases(scene), scene.environment, BrdfLut.build())
+    for c in cams:
+        r.render(c)
+    r.reserve(cams[0], int(r.entries_needed() * 2) + 4096)
+    ref = [(c_, g_.planar.clone()) for c_, g_ in (
+        (lambda o: (o[0].clone(), o[1]))(r.render(c, check=True)) for c in cams)]
+    for (col_ref, gb_ref), c in zip(ref, cams):
+        col, gb = r.render(c, check=False)
+        assert torch.equal(col, col_ref)
+        assert torch.equal(gb.planar, gb_ref)
+    other = synth.bench_cameras(1, 64, 64)[0]
+    import ctypes as C
+    from paper_2506_13348_b200 import _lib
+    h, _ = r._graph(cams[0], 96, 80)
+    with pytest.raises(ValueError):
+        _lib.check(_lib.lib().tsb_frame_graph_launch(h, C.byref(_lib.camera_struct(other)), None,
+                                                     None), "graph")
+    r.close()
