@@ -305,6 +305,27 @@ int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step
 int tsb_orthonormalize_tangents(int32_t num_splats, double* tangent_u, double* tangent_v,
                                 void* stream);
 
+/* ---- Environment precompute (K15-K17) ---------------------------------- */
+
+/* Scratch bytes of tsb_env_prefilter for a height x width base map. */
+int tsb_env_scratch_size(int32_t height, int32_t width, uint64_t* bytes);
+
+/* EnvironmentLight.from_base (environment.py:231-244) on the device: from a
+ * float64 base radiance map (height x width x 3, device), level 0 = the base
+ * (float32), level l >= 1 = GGX prefilter with roughness l/(levels-1)
+ * (prefilter_specular :145-175) at mip_h[l] x mip_w[l], and the cosine
+ * irradiance (diffuse_irradiance :178-195) at diff_h x diff_w, all over the
+ * 2x-downsampled base, fp64 sums. Outputs float32 x 3; any may be NULL. */
+int tsb_env_prefilter(const double* base, int32_t height, int32_t width, int32_t levels,
+                      float* const* spec_mips, const int32_t* mip_h, const int32_t* mip_w,
+                      float* diffuse, int32_t diff_h, int32_t diff_w, void* scratch,
+                      uint64_t scratch_bytes, void* stream);
+
+/* BrdfLut.build (environment.py:381-425) on the device: table (resolution x
+ * resolution x 2, float64, device) of split-sum (A, B), GGX importance
+ * sampling over `samples` Hammersley points per cell. */
+int tsb_brdf_lut(int32_t resolution, int32_t samples, double* table, void* stream);
+
 /* Last error message of the calling thread. */
 const char* tsb_last_error(void);
 

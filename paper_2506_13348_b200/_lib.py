@@ -125,6 +125,11 @@ _SIGNATURES = {
                                _P, _P, C.POINTER(C.c_void_p)],
     "tsb_frame_graph_launch": [_P, C.POINTER(Camera_t), _P, _P],
     "tsb_frame_graph_destroy": [_P],
+    "tsb_env_scratch_size": [C.c_int32, C.c_int32, C.POINTER(C.c_uint64)],
+    "tsb_env_prefilter": [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p),
+                          C.POINTER(C.c_int32), C.POINTER(C.c_int32), _P, C.c_int32, C.c_int32,
+                          _P, C.c_uint64, _P],
+    "tsb_brdf_lut": [C.c_int32, C.c_int32, _P, _P],
 }
 
 _lib = None

@@ -104,9 +104,15 @@ class EnvironmentLight:
         return len(self.spec_mips)
 
     @staticmethod
-    def from_base(base, levels: int = 6, diffuse_height: int = 32) -> "EnvironmentLight":
+    def from_base(base, levels: int = 6, diffuse_height: int = 32,
+                  device=None) -> "EnvironmentLight":
         """Level l is max(4, h>>l) x max(8, w>>l) at roughness l/(levels-1)
-        (environment.py:231-244)."""
+        (environment.py:231-244). With `device` the quadratures run on the
+        GPU (K15-K16, tsb_env_prefilter; fp64 sums in another order, so
+        float32-rounding-level differences); without, this host restatement
+        is bit-identical to the reference."""
+        if device is not None:
+            return EnvironmentLight._from_base_device(base, levels, diffuse_height, device)
         base = np.asarray(base, dtype=np.float64)
         h, w = base.shape[:2]
         mips = [base.astype(np.float32)]
@@ -115,6 +121,35 @@ class EnvironmentLight:
                                            max(8, w >> level)).astype(np.float32))
         dh = min(diffuse_height, h)
         return EnvironmentLight(mips, diffuse_irradiance(base, dh, 2 * dh).astype(np.float32))
+
+    @staticmethod
+    def _from_base_device(base, levels, diffuse_height, device):
+        import ctypes as C
+
+        import torch
+
+        from . import _lib
+        b = torch.as_tensor(np.ascontiguousarray(base, np.float64), device=device)
+        h, w = int(b.shape[0]), int(b.shape[1])
+        if not 1 <= levels <= _lib.ENV_MAX_LEVELS:
+            raise ValueError("levels out of range")
+        hs = [h] + [max(4, h >> l) for l in range(1, levels)]
+        ws = [w] + [max(8, w >> l) for l in range(1, levels)]
+        mips = [torch.empty((hh, ww, 3), dtype=torch.float32, device=device)
+                for hh, ww in zip(hs, ws)]
+        dh = min(diffuse_height, h)
+        diff = torch.empty((dh, 2 * dh, 3), dtype=torch.float32, device=device)
+        L = _lib.lib()
+        nb = C.c_uint64()
+        _lib.check(L.tsb_env_scratch_size(h, w, C.byref(nb)), "tsb_env_scratch_size")
+        scratch = torch.empty(int(nb.value), dtype=torch.uint8, device=device)
+        ptrs = (C.c_void_p * levels)(*[_lib.ptr(m) for m in mips])
+        _lib.check(L.tsb_env_prefilter(_lib.ptr(b), h, w, levels, ptrs,
+                                       (C.c_int32 * levels)(*hs), (C.c_int32 * levels)(*ws),
+                                       _lib.ptr(diff), dh, 2 * dh, _lib.ptr(scratch),
+                                       int(nb.value), _lib.stream_handle()), "tsb_env_prefilter")
+        torch.cuda.current_stream().synchronize()
+        return EnvironmentLight([m.cpu().numpy() for m in mips], diff.cpu().numpy())
 
     @staticmethod
     def constant(value, height: int = 64, levels: int = 6) -> "EnvironmentLight":
@@ -166,7 +201,21 @@ class BrdfLut:
         return self.table.shape[0]
 
     @staticmethod
-    def build(resolution: int = 64, samples: int = 2048) -> "BrdfLut":
+    def build(resolution: int = 64, samples: int = 2048, device=None) -> "BrdfLut":
+        """BrdfLut.build (environment.py:381-390). With `device` the table is
+        integrated on the GPU (K17, tsb_brdf_lut)."""
+        if device is not None:
+            import torch
+
+            from . import _lib
+            t = torch.empty((resolution, resolution, 2), dtype=torch.float64, device=device)
+            _lib.check(_lib.lib().tsb_brdf_lut(resolution, samples, _lib.ptr(t),
+                                               _lib.stream_handle()), "tsb_brdf_lut")
+            return BrdfLut(t.cpu().numpy())
+        return BrdfLut._build_host(resolution, samples)
+
+    @staticmethod
+    def _build_host(resolution: int = 64, samples: int = 2048) -> "BrdfLut":
         xi = hammersley(samples)
         phi = TWO_PI * xi[:, 0]
         cphi, sphi = np.cos(phi), np.sin(phi)
