@@ -326,6 +326,16 @@ int tsb_env_prefilter(const double* base, int32_t height, int32_t width, int32_t
  * sampling over `samples` Hammersley points per cell. */
 int tsb_brdf_lut(int32_t resolution, int32_t samples, double* table, void* stream);
 
+/* K14: the decomposition images of the render command (cli.py:52-96 with
+ * --decompose) as 8-bit pixels: out holds, back to back, albedo (H x W x 3),
+ * normal (H x W x 3), roughness (H x W), metallic (H x W), diffuse,
+ * specular and final (H x W x 3 each) — 17 W H bytes — quantised like
+ * write_png (imgio.py:13-21) after linear_to_display where the reference
+ * applies it. gbuf planar 13 x H x W; colour/diffuse/specular H x W x 3. */
+int tsb_decompose(const float* gbuf, const float* color, const float* diffuse,
+                  const float* specular, int32_t width, int32_t height, uint8_t* out,
+                  void* stream);
+
 /* Last error message of the calling thread. */
 const char* tsb_last_error(void);
 

@@ -130,6 +130,7 @@ _SIGNATURES = {
                           C.POINTER(C.c_int32), C.POINTER(C.c_int32), _P, C.c_int32, C.c_int32,
                           _P, C.c_uint64, _P],
     "tsb_brdf_lut": [C.c_int32, C.c_int32, _P, _P],
+    "tsb_decompose": [_P, _P, _P, _P, C.c_int32, C.c_int32, _P, _P],
 }
 
 _lib = None

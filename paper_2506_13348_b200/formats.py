@@ -220,6 +220,7 @@ def load_scene(path) -> Scene:
                                read_pfm(_require(directory, e["diffuse"])))
     if "mesh" in meta:
         raise NotImplementedError("mesh visibility is outside the B200 render path")
+    pos, tu, tv, sc, op, sh, texels = (np.array(a) for a in (pos, tu, tv, sc, op, sh, texels))
     return Scene(pos, tu, tv, sc, op, sh, int(meta["sh_degree"]), texels,
                  TextureConfig(t_res, float(meta["texture_support"])), env, None,
                  np.asarray(meta["background"], dtype=np.float64))

@@ -28,3 +28,13 @@ np.savez_compressed(
     spec0=scene.environment.spec_mips[0], diffuse=scene.environment.diffuse,
     background=scene.background, cam0=cams[0].world_to_view, cam1=cams[1].world_to_view)
 print("ok", scene.num_splats)
+
+# reference `render --decompose` of the checkpoint (default camera), both
+# texture modes: the 8-bit images the CLI test compares against
+from texsplat.cli import main as ref_main  # noqa: E402
+
+for mode, extra in (("perprim", []), ("atlas", ["--atlas"])):
+    out = HERE / f"io_render_{mode}"
+    shutil.rmtree(out, ignore_errors=True)
+    ref_main(["render", "--scene", str(HERE / "io_ckpt"), "--decompose", "--out", str(out)]
+             + extra)
