@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
     const int by0 = (tile / p.tiles_x) * TILE + (blk / wx) * 4;
     if (bx0 >= p.W || by0 >= p.H) continue;
     const int bx1 = min(bx0 + 8, p.W), by1 = min(by0 + 4, p.H);
+    const BlockBox bb = tsb_block_box(p.cam, bx0, by0, bx1, by1);
     const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
     const bool inside = px < p.W && py < p.H;
     const int pix = py * p.W + px;
@@ -422,10 +423,16 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
       const int cnt = hi - lo + 1;
       // ---- stage the step [lo, hi]
       __syncwarp();
-      bool hit = false;
+      bool hit = false, full = false;
       if (lane < cnt) {
         const int id = __ldg(p.evals + lo + lane);
-        hit = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, ws.lin) != 0;
+        float4 gv[4];
+        hit = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, bb, p.near_f, full,
+                             gv) != 0;
+        const float gl[11] = {gv[0].x, gv[0].y, gv[0].z, gv[0].w, gv[1].x, gv[1].y,
+                              gv[1].z, gv[1].w, gv[2].x, gv[2].y, gv[2].z};
+#pragma unroll
+        for (int c = 0; c < 11; ++c) ws.lin[c][lane] = gl[c];
         ws.sid[lane] = id;
         const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
         const float4 m0 = __ldg(mq), m1 = __ldg(mq + 1), m2 = __ldg(mq + 2), m3 = __ldg(mq + 3);
@@ -439,6 +446,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
         for (int c = 0; c < 9; ++c) ws.mf[c][lane] = (float)__ldg(m64 + c);
       }
       const uint32_t cand = __ballot_sync(0xffffffffu, hit);
+      const uint32_t fullm = __ballot_sync(0xffffffffu, full);
       __syncwarp();
       if (!cand) continue;
       // ---- decide: this pixel's contributors in the step (entries <= last)
@@ -447,8 +455,13 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
         const int nv = last - lo + 1;
         const uint32_t valid = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
         // uniform candidate loop (broadcast reads), masked afterwards
-        live = tsb_decide_step(ws.dec, ws.lin, ws.sid, cand, lane, x, y, p.near_f, p.cam, p.m64,
-                               px, py) & valid;
+        auto load_lin = [&](int k, float* L) {
+#pragma unroll
+          for (int c = 0; c < 11; ++c) L[c] = ws.lin[c][k];
+          L[11] = ws.dec[k].r2hi;
+        };
+        live = (fullm | tsb_decide_step(ws.dec, load_lin, ws.sid, cand & ~fullm, lane, x, y,
+                                        p.near_f, p.cam, p.m64, px, py)) & valid;
       }
       // ---- adjoint, back to front over the entries with a live pixel
       for (uint32_t any = __reduce_or_sync(0xffffffffu, live); any;) {

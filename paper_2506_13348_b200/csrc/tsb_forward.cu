@@ -341,6 +341,7 @@ struct RasterParams {
   const double* m64;
   // texture sources
   int32_t T, page_w, tstride;
+  float t6, t2, tmh;  // T/6, T/2, T-1/2 (HW-mode texel coordinates)
   const float4* fam_a;
   const float4* fam_b;
   const float* flat;
@@ -357,70 +358,45 @@ struct RasterParams {
   const int32_t* tile_order;  // tiles by descending list length (may be null)
 };
 
-// A fragment's texel data in flight: the two atlas families (HW / verify)
-// or the flat attributes, plus the fragment's u, v, z, alpha.
-struct Frag {
-  float4 A, B;
-  float z, a;
-};
-
-// Issue the texel reads of fragment (u, v) of splat material `m`. In HW mode
-// these are two bilinear tex2DLayered fetches; verify mode reads the four
-// corners of both families and applies tsb_lerp4 (== lerp_corners).
-template <int MODE>
-__device__ __forceinline__ void frag_fetch(const RasterParams& p, const MatRec& m, int id,
-                                           float u, float v, Frag& f) {
-  if (MODE == TSB_MODE_FLAT) {
-    const float* fl = p.flat + 5 * id;
-    f.A = make_float4(__ldg(fl), __ldg(fl + 1), __ldg(fl + 2), __ldg(fl + 4));
-    f.B = make_float4(0.f, 0.f, __ldg(fl + 3), 0.f);
-    return;
-  }
-  tsb_texc tc;
-  tsb_texel_coords(u, v, p.T, &tc);
-  if (MODE == TSB_MODE_HW) {
-    const float sx = m.tex_x + tc.xs + 0.5f;
-    const float sy = m.tex_y + tc.yt + 0.5f;
-    f.A = tex2DLayered<float4>(p.tex_a, sx, sy, m.page);
-    f.B = tex2DLayered<float4>(p.tex_b, sx, sy, m.page);
-  } else {
-    const int S = p.tstride;
-    const int r0 = m.lin_off + tc.j0 * p.page_w, r1 = m.lin_off + tc.j1 * p.page_w;
-    const float4 a00 = __ldg(p.fam_a + S * (r0 + tc.i0)), a01 = __ldg(p.fam_a + S * (r0 + tc.i1));
-    const float4 a10 = __ldg(p.fam_a + S * (r1 + tc.i0)), a11 = __ldg(p.fam_a + S * (r1 + tc.i1));
-    const float4 b00 = __ldg(p.fam_b + S * (r0 + tc.i0)), b01 = __ldg(p.fam_b + S * (r0 + tc.i1));
-    const float4 b10 = __ldg(p.fam_b + S * (r1 + tc.i0)), b11 = __ldg(p.fam_b + S * (r1 + tc.i1));
-    f.A.x = tsb_lerp4(a00.x, a01.x, a10.x, a11.x, tc.fs, tc.ft);
-    f.A.y = tsb_lerp4(a00.y, a01.y, a10.y, a11.y, tc.fs, tc.ft);
-    f.A.z = tsb_lerp4(a00.z, a01.z, a10.z, a11.z, tc.fs, tc.ft);
-    f.A.w = tsb_lerp4(a00.w, a01.w, a10.w, a11.w, tc.fs, tc.ft);
-    f.B.x = tsb_lerp4(b00.x, b01.x, b10.x, b11.x, tc.fs, tc.ft);
-    f.B.y = tsb_lerp4(b00.y, b01.y, b10.y, b11.y, tc.fs, tc.ft);
-    f.B.z = tsb_lerp4(b00.z, b01.z, b10.z, b11.z, tc.fs, tc.ft);
-    f.B.w = 0.f;
-  }
+// tsb_decode_normal with the SFU's approximate square roots (HW-texture mode
+// only, whose texels are already filtered with 8-bit weights; verify mode
+// keeps the correctly rounded path that matches the oracle bit for bit).
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
-
-// Attribute row x (rasterize.py:261-317 channel order) and composite.
-template <int MODE>
-__device__ __forceinline__ float frag_composite(const MatRec& m, const Frag& f, float* acc,
-                                                float T) {
-  float xa[12];
-  xa[0] = f.A.x; xa[1] = f.A.y; xa[2] = f.A.z;
-  xa[3] = f.B.z;  // metallic
-  xa[4] = f.A.w;  // roughness
-  if (MODE == TSB_MODE_FLAT) {
-    xa[5] = m.frame[6]; xa[6] = m.frame[7]; xa[7] = m.frame[8];
-  } else {
-    tsb_decode_normal(f.B.x, f.B.y, m.frame, xa + 5);
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void tsb_decode_normal_approx(float ea, float eb, const float* frame,
+                                                         float* nw) {
+  float nx = fmaf(2.0f, ea, -1.0f);
+  float ny = fmaf(2.0f, eb, -1.0f);
+  const float d2 = fmaf(nx, nx, ny * ny);
+  if (d2 > 1.0f) {
+    const float sc = rsqrt_approx(d2);
+    nx *= sc;
+    ny *= sc;
   }
-  xa[8] = m.l_ind[0]; xa[9] = m.l_ind[1]; xa[10] = m.l_ind[2];
-  xa[11] = f.z;
-  return tsb_composite(acc, xa, f.a, T);
+  const float q = fmaf(-nx, nx, fmaf(-ny, ny, 1.0f));
+  const float nz = sqrt_approx(fmaxf(q, 0.0f));
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    nw[i] = fmaf(nz, frame[6 + i], fmaf(ny, frame[3 + i], nx * frame[i]));
 }
 
 #ifndef TSB_PAIR_ILP
 #define TSB_PAIR_ILP 2
+#endif
+
+#ifdef TSB_STATS
+// Work counters of k_raster_fwd (instrumented builds only: make EXTRA=-DTSB_STATS):
+// 0 units, 1 steps, 2 candidates, 3 block-full candidates, 5 pair iterations,
+// 6 composited pairs, 8 undone lanes at decide, 9 live pairs, 10 undone lanes x candidates.
+__device__ unsigned long long g_tsb_stats[16];
 #endif
 
 // Warp-private shared memory of the rasterizer.
@@ -428,14 +404,14 @@ struct WarpSmem {
   // staged step, AoS for the decide loop (all lanes read the same splat)
   DecRec dec[32];
   int32_t sid[32];            // splat ids
-  // the same step as structure-of-arrays for texturing / blending, where
-  // every lane reads a different splat: conflict-free 32-bit loads
-  float lin[11][32];          // intersection forms L0..L10
-  float frame[9][32];         // t_u, t_v, t_u x t_v
-  float texo[2][32];          // chart origin (texels)
-  int32_t page[32];
-  int32_t loff[32];
-  float lind[3][32];          // clamped SH radiance
+  // the same step for texturing / blending, one 112-byte record per entry
+  // read with 128-bit loads (7 x 16 B: the stride is odd in 16-byte units, so
+  // lanes reading different entries of one quarter-warp rarely share banks):
+  //   [0] L0..L3  [1] L4..L7  [2] L8, det, opacity, r2hi   (intersection forms)
+  //   [3] chart origin x, y (texels), page, linear offset
+  //   [4] frame 0..3  [5] frame 4..7  [6] frame 8, clamped SH radiance rgb
+  float4 rec[32][7];
+  BlockBox bb;                // the current unit's block (read by the stage step)
 };
 constexpr size_t kRasterWarpSmem = (sizeof(WarpSmem) + 15) & ~size_t(15);
 
@@ -453,9 +429,8 @@ template <int MODE>
 __device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem& ws, int q,
                                            float2 xy, PairFetch& f) {
   const int k = q & 31;
-  float L[11];
-#pragma unroll
-  for (int c = 0; c < 11; ++c) L[c] = ws.lin[c][k];
+  const float4 r0 = ws.rec[k][0], r1 = ws.rec[k][1], r2 = ws.rec[k][2], r3 = ws.rec[k][3];
+  const float L[11] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z};
   float u, v;
   tsb_uvza_lin(L, xy.x, xy.y, &u, &v, &f.z, &f.a);
   f.k = k;
@@ -465,12 +440,14 @@ __device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem
     f.B = make_float4(0.f, 0.f, __ldg(fl + 3), 0.f);
     return;
   }
-  tsb_texc tc;
-  tsb_texel_coords(u, v, p.T, &tc);
   if (MODE == TSB_MODE_HW) {
-    const float sx = ws.texo[0][k] + tc.xs + 0.5f;
-    const float sy = ws.texo[1][k] + tc.yt + 0.5f;
-    const int page = ws.page[k];
+    // texture-unit coordinates of the reference footprint (textures.py:152-200):
+    // xs = clamp(clamp((u+3)/6, h, 1-h) T - 0.5, 0, T-1), sampled at xs + 0.5,
+    // i.e. chart origin + clamp(u T/6 + T/2, 1/2, T - 1/2) (the filter's own
+    // 8-bit weights dominate the rounding difference; tolerance-checked mode)
+    const float sx = r3.x + fminf(fmaxf(fmaf(u, p.t6, p.t2), 0.5f), p.tmh);
+    const float sy = r3.y + fminf(fmaxf(fmaf(v, p.t6, p.t2), 0.5f), p.tmh);
+    const int page = __float_as_int(r3.z);
 #ifdef TSB_PROBE_NOTEX
     f.A = make_float4(sx * 1e-9f, 0.5f, 0.5f, 0.5f);
     f.B = make_float4(0.5f, sy * 1e-9f + 0.5f, 0.2f, 0.f);
@@ -479,8 +456,10 @@ __device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem
     f.B = tex2DLayered<float4>(p.tex_b, sx, sy, page);
 #endif
   } else {
+    tsb_texc tc;
+    tsb_texel_coords(u, v, p.T, &tc);
     const int S = p.tstride;
-    const int loff = ws.loff[k];
+    const int loff = __float_as_int(r3.w);
     const int r0 = loff + tc.j0 * p.page_w, r1 = loff + tc.j1 * p.page_w;
     const float4 a00 = __ldg(p.fam_a + S * (r0 + tc.i0)), a01 = __ldg(p.fam_a + S * (r0 + tc.i1));
     const float4 a10 = __ldg(p.fam_a + S * (r1 + tc.i0)), a11 = __ldg(p.fam_a + S * (r1 + tc.i1));
@@ -501,12 +480,13 @@ __device__ __forceinline__ void pair_issue(const RasterParams& p, const WarpSmem
 // row into result slot t.
 template <int MODE>
 __device__ __forceinline__ void pair_result(const WarpSmem& ws, const PairFetch& f, float* rv) {
-  float fr[9];
-#pragma unroll
-  for (int c = 0; c < 9; ++c) fr[c] = ws.frame[c][f.k];
+  const float4 r4 = ws.rec[f.k][4], r5 = ws.rec[f.k][5], r6 = ws.rec[f.k][6];
+  const float fr[9] = {r4.x, r4.y, r4.z, r4.w, r5.x, r5.y, r5.z, r5.w, r6.x};
   float nw[3];
   if (MODE == TSB_MODE_FLAT) {
     nw[0] = fr[6]; nw[1] = fr[7]; nw[2] = fr[8];
+  } else if (MODE == TSB_MODE_HW) {
+    tsb_decode_normal_approx(f.B.x, f.B.y, fr, nw);
   } else {
     tsb_decode_normal(f.B.x, f.B.y, fr, nw);
   }
@@ -520,6 +500,9 @@ __device__ __forceinline__ void pair_result(const WarpSmem& ws, const PairFetch&
   rv[7] = nw[2];
   rv[8] = f.z;
   rv[9] = f.a;
+  rv[10] = r6.y;  // clamped SH radiance
+  rv[11] = r6.z;
+  rv[12] = r6.w;
 }
 
 
@@ -561,6 +544,9 @@ k_raster_fwd(RasterParams p) {
     if (lane == 0) unit = atomicAdd(p.work_counter, 1);
     unit = __shfl_sync(0xffffffffu, unit, 0);
     if (unit >= num_units) break;
+#ifdef TSB_STATS
+    if (lane == 0) atomicAdd(&g_tsb_stats[0], 1ull);
+#endif
     const int tile = p.tile_order ? p.tile_order[unit / NBLK] : unit / NBLK;
     const int blk = unit % NBLK;
     const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
@@ -572,6 +558,10 @@ k_raster_fwd(RasterParams p) {
     const bool inside = px < p.W && py < p.H;
     const float x = (float)tsb_pixel_x(&p.cam, px), y = (float)tsb_pixel_y(&p.cam, py);
     const int bx1 = min(bx0 + 8, p.W), by1 = min(by0 + 4, p.H);
+    __syncwarp();
+    if (lane == 0) ws.bb = tsb_block_box(p.cam, bx0, by0, bx1, by1);
+    __syncwarp();
+    const BlockBox& bb = ws.bb;
 
     float acc[13];
 #pragma unroll
@@ -584,32 +574,55 @@ k_raster_fwd(RasterParams p) {
       if (__all_sync(0xffffffffu, done)) break;
       // ---- stage
       const int e = base + lane;
-      bool hit = false;
+      bool hit = false, full = false;
       __syncwarp();
       if (e < end) {
         const int id = __ldg(p.evals + e);
-        const uint32_t pm = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, ws.lin);
+        float4 gv[4];
+        const uint32_t pm = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, bb,
+                                           p.near_f, full, gv);
         hit = pm != 0;
         ws.sid[lane] = id;
         const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
-        const float4 m0 = __ldg(mq), m1 = __ldg(mq + 1), m2 = __ldg(mq + 2), m3 = __ldg(mq + 3);
-        ws.frame[0][lane] = m0.x; ws.frame[1][lane] = m0.y; ws.frame[2][lane] = m0.z;
-        ws.frame[3][lane] = m0.w; ws.frame[4][lane] = m1.x; ws.frame[5][lane] = m1.y;
-        ws.frame[6][lane] = m1.z; ws.frame[7][lane] = m1.w; ws.frame[8][lane] = m2.x;
-        ws.lind[0][lane] = m2.y; ws.lind[1][lane] = m2.z; ws.lind[2][lane] = m2.w;
-        ws.texo[0][lane] = m3.x; ws.texo[1][lane] = m3.y;
-        ws.page[lane] = __float_as_int(m3.z); ws.loff[lane] = __float_as_int(m3.w);
+        float4* rec = ws.rec[lane];
+        rec[0] = gv[0]; rec[1] = gv[1]; rec[2] = gv[2];
+        rec[4] = __ldg(mq); rec[5] = __ldg(mq + 1); rec[6] = __ldg(mq + 2); rec[3] = __ldg(mq + 3);
       }
       const uint32_t cand = __ballot_sync(0xffffffffu, hit);
+      const uint32_t fullm = __ballot_sync(0xffffffffu, full);
       __syncwarp();
       if (!cand) continue;
-      // ---- decide
+      // ---- decide (splats surely live on the whole block need no per-pixel test)
       uint32_t live = 0;
       if (!done)
-        live = tsb_decide_step(ws.dec, ws.lin, ws.sid, cand, lane, x, y, p.near_f, p.cam, p.m64,
-                               px, py);
+        live = fullm | tsb_decide_step(
+                           ws.dec,
+                           [&](int k, float* L) {
+                             const float4 a = ws.rec[k][0], b = ws.rec[k][1], c = ws.rec[k][2];
+                             L[0] = a.x; L[1] = a.y; L[2] = a.z; L[3] = a.w;
+                             L[4] = b.x; L[5] = b.y; L[6] = b.z; L[7] = b.w;
+                             L[8] = c.x; L[9] = c.y; L[10] = c.z; L[11] = c.w;
+                           },
+                           ws.sid, cand & ~fullm, lane, x, y, p.near_f, p.cam, p.m64, px, py);
+#ifdef TSB_STATS
+      {
+        const uint32_t nd = __ballot_sync(0xffffffffu, !done);
+        const int lv = __reduce_add_sync(0xffffffffu, (unsigned)__popc(live));
+        if (lane == 0) {
+          atomicAdd(&g_tsb_stats[1], 1ull);
+          atomicAdd(&g_tsb_stats[2], (unsigned long long)__popc(cand));
+          atomicAdd(&g_tsb_stats[3], (unsigned long long)__popc(fullm));
+          atomicAdd(&g_tsb_stats[8], (unsigned long long)__popc(nd));
+          atomicAdd(&g_tsb_stats[9], (unsigned long long)lv);
+          atomicAdd(&g_tsb_stats[10], (unsigned long long)__popc(nd) * __popc(cand));
+        }
+      }
+#endif
       // ---- texture + blend, in order, TSB_PAIR_ILP live pairs per lane per iteration
       while (__any_sync(0xffffffffu, live != 0)) {
+#ifdef TSB_STATS
+        if (lane == 0) atomicAdd(&g_tsb_stats[5], 1ull);
+#endif
         if (live) {
           int kk[TSB_PAIR_ILP];
           bool hv[TSB_PAIR_ILP];
@@ -625,17 +638,20 @@ k_raster_fwd(RasterParams p) {
           for (int j = 0; j < TSB_PAIR_ILP; ++j) {
             if (hv[j] && !done) {
               const int k = kk[j];
-              float rv[10];
+              float rv[13];
               pair_result<MODE>(ws, f[j], rv);
               float xa[12];
 #pragma unroll
               for (int c = 0; c < 8; ++c) xa[c] = rv[c];
-              xa[8] = ws.lind[0][k]; xa[9] = ws.lind[1][k]; xa[10] = ws.lind[2][k];
+              xa[8] = rv[10]; xa[9] = rv[11]; xa[10] = rv[12];
               xa[11] = rv[8];
               T_last = T;
               T = tsb_composite(acc, xa, rv[9], T);
               ++n;
               last = base + k;
+#ifdef TSB_STATS
+              atomicAdd(&g_tsb_stats[6], 1ull);
+#endif
               if (p.touched) p.touched[ws.sid[k]] = 1;
               if (!(T > teps)) { done = true; live = 0; }
             }
@@ -942,6 +958,9 @@ int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera, const
   rp.m64 = ws_ptr<double>(ws, L.m64);
   rp.T = atlas->resolution; rp.page_w = atlas->page_w;
   rp.tstride = atlas->texel_stride > 0 ? atlas->texel_stride : 1;
+  rp.t6 = (float)atlas->resolution / 6.0f;
+  rp.t2 = 0.5f * (float)atlas->resolution;
+  rp.tmh = (float)atlas->resolution - 0.5f;
   rp.fam_a = reinterpret_cast<const float4*>(atlas->family_a);
   rp.fam_b = reinterpret_cast<const float4*>(atlas->family_b);
   rp.flat = atlas->flat_attrs;
@@ -1126,6 +1145,17 @@ int tsb_atlas_tex_destroy(tsb_atlas_tex_t h) {
   delete t;
   return TSB_OK;
 }
+
+#ifdef TSB_STATS
+int tsb_debug_stats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, tsb::g_tsb_stats, sizeof(unsigned long long) * 16);
+  if (reset) {
+    static const unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(tsb::g_tsb_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 int tsb_tex_probe(tsb_atlas_tex_t h, int32_t window, int32_t iters, float* sink, int32_t blocks,
                   int32_t threads, void* stream) {

@@ -58,10 +58,11 @@ __device__ __forceinline__ uint32_t tsb_block_pixmask(uint32_t gbx, uint32_t gby
 // Live bits of one pixel (this lane) over the candidate mask `m` of a
 // staged step: the division-free pre-decision, two candidates per
 // iteration (independent chains), then the exact fp32 path and the fp64
-// guard band for the rare undecided pairs. `lin` is the step's [11][32]
-// structure-of-arrays copy of L0..L10, `sid` its splat ids. The result is
-// exactly tsb_eval_lin + tsb_live_f64 of every candidate (tsb_math.h).
-__device__ __forceinline__ uint32_t tsb_decide_step(const DecRec* dec, const float (*lin)[32],
+// guard band for the rare undecided pairs. `load_lin(k, L)` fills L[0..11]
+// (tsb_make_lin's words) of staged entry k, `sid` holds the splat ids. The
+// result is exactly tsb_eval_lin + tsb_live_f64 of every candidate (tsb_math.h).
+template <class LoadLin>
+__device__ __forceinline__ uint32_t tsb_decide_step(const DecRec* dec, LoadLin load_lin,
                                                     const int32_t* sid, uint32_t m, int lane,
                                                     float x, float y, float near_f,
                                                     const tsb_cam_params& cam, const double* m64,
@@ -86,9 +87,7 @@ __device__ __forceinline__ uint32_t tsb_decide_step(const DecRec* dec, const flo
   for (uint32_t u = undecided; u; u &= u - 1) {
     const int k = __ffs(u) - 1;
     float L[12];
-#pragma unroll
-    for (int c = 0; c < 11; ++c) L[c] = lin[c][k];
-    L[11] = dec[k].r2hi;
+    load_lin(k, L);
     float uu, vv, z, a;
     int r = tsb_eval_lin(L, x, y, near_f, &uu, &vv, &z, &a);
     if (r == 2) {
@@ -100,23 +99,101 @@ __device__ __forceinline__ uint32_t tsb_decide_step(const DecRec* dec, const flo
   return live;
 }
 
-// Stage splat `id` of a step into lane slot `lane`: the decide record (AoS)
-// and the structure-of-arrays intersection forms. Returns the pixel mask.
+// Camera-plane extent of a warp's 8x4 pixel block (clipped to the image):
+// the fp32 pixel coordinates x(bx0), x(bx1-1), y(by0), y(by1-1) — exactly the
+// values the block's lanes evaluate at its corners — and the block's pixel mask.
+struct BlockBox {
+  float x0, y0, dx, dy;  // corner (x0, y0) and the extents to the opposite corner
+  float X, Y;            // max |x|, |y| over the block
+  uint32_t valid;
+};
+
+__device__ __forceinline__ BlockBox tsb_block_box(const tsb_cam_params& cam, int bx0, int by0,
+                                                  int bx1, int by1) {
+  BlockBox b;
+  const float xa = (float)tsb_pixel_x(&cam, bx0), xb = (float)tsb_pixel_x(&cam, bx1 - 1);
+  const float ya = (float)tsb_pixel_y(&cam, by0), yb = (float)tsb_pixel_y(&cam, by1 - 1);
+  b.x0 = xa; b.dx = xb - xa;
+  b.y0 = ya; b.dy = yb - ya;
+  b.X = fmaxf(fabsf(xa), fabsf(xb));
+  b.Y = fmaxf(fabsf(ya), fabsf(yb));
+  b.valid = tsb_block_pixmask((uint32_t)bx0 | ((uint32_t)bx1 << 16),
+                              (uint32_t)by0 | ((uint32_t)by1 << 16), bx0, by0, bx1, by1);
+  return b;
+}
+
+// Block-level "surely live": true only if tsb_predecide_lin_nb returns 1 (live)
+// at EVERY fp32 pixel point (x, y) of the block rectangle, so the warp can set
+// the splat's live bit for all its pixels without evaluating them. A
+// performance shortcut that never changes a decision. With S_F = |a|X+|b|Y+|c|
+// for a form F = a x + b y + c (X, Y = max |x|, |y| on the block):
+//  * e_F = 2^-21 S_F bounds the error of F's fp32 value at a pixel (two
+//    roundings: 2^-23 S_F) and at the corners, which are stepped from
+//    (x0, y0) by one or two more fmaf's with the rounded extents dx, dy.
+//  * D is affine: with every corner |D~| > eD of one sign, the exact D keeps
+//    that sign on the block and |D| >= dlo = min |D~_c| - eD there.
+//  * (x,y) -> (u,v) = (Nu/D, Nv/D) is projective without a pole on the block,
+//    so the block maps onto the convex quad of its corner images: the exact
+//    |(u,v)| on the block is at most its largest corner value rho.
+//  * corner test q~_c <= 0.8999 r2lo (|D~_c| - eD)^2 and eN <= 0.01 sqrt(r2lo) dlo
+//    (eN = e_Nu + e_Nv) give rho <= 0.9587 sqrt(r2lo); with eD <= 0.03 dlo the
+//    per-pixel fp32 N~ <= rho|D| + eN stays below 0.99999 sqrt(r2lo)(|D| - eD),
+//    so the pixel's own q <= r2lo D^2 (three roundings) holds; q <= r2hi D^2 too.
+//  * z: zs > zt holds with a 3e-5 relative margin at the largest pixel |D~|.
+// The GPU-vs-oracle bit-exact tests (tests/test_gpu_forward.py) check it.
+__device__ __forceinline__ bool tsb_block_surely_live(const float4& g0, const float4& g1,
+                                                      const float4& g2, float r2lo,
+                                                      const BlockBox& b, float near_z) {
+  // L0..L8 = D, Nu, Nv coefficients, L9 = det (tsb_make_lin)
+  const float k21 = 4.76837158203125e-7f;  // 2^-21
+  const float eD = k21 * fmaf(fabsf(g0.x), b.X, fmaf(fabsf(g0.y), b.Y, fabsf(g0.z)));
+  const float eN = k21 * (fmaf(fabsf(g0.w), b.X, fmaf(fabsf(g1.x), b.Y, fabsf(g1.y))) +
+                          fmaf(fabsf(g1.z), b.X, fmaf(fabsf(g1.w), b.Y, fabsf(g2.x))));
+  float D[4], U[4], V[4];
+  D[0] = fmaf(g0.x, b.x0, fmaf(g0.y, b.y0, g0.z));
+  U[0] = fmaf(g0.w, b.x0, fmaf(g1.x, b.y0, g1.y));
+  V[0] = fmaf(g1.z, b.x0, fmaf(g1.w, b.y0, g2.x));
+  D[1] = fmaf(g0.x, b.dx, D[0]); U[1] = fmaf(g0.w, b.dx, U[0]); V[1] = fmaf(g1.z, b.dx, V[0]);
+  D[2] = fmaf(g0.y, b.dy, D[0]); U[2] = fmaf(g1.x, b.dy, U[0]); V[2] = fmaf(g1.w, b.dy, V[0]);
+  D[3] = fmaf(g0.y, b.dy, D[1]); U[3] = fmaf(g1.x, b.dy, U[1]); V[3] = fmaf(g1.w, b.dy, V[1]);
+  const float c = 0.8999f * r2lo;
+  bool pos = true, neg = true, in = true;
+  float dmin = 3.0e38f, dmax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    pos = pos && D[i] > eD;
+    neg = neg && D[i] < -eD;
+    const float aD = fabsf(D[i]);
+    dmin = fminf(dmin, aD);
+    dmax = fmaxf(dmax, aD);
+    const float t = aD - eD;
+    in = in && fmaf(U[i], U[i], V[i] * V[i]) <= (t * t) * c;
+  }
+  const float dlo = dmin - eD;
+  const float dhi = dmax + 2.f * eD;
+  const float zl = pos ? g2.y : -g2.y;
+  return (pos || neg) && in && dlo > 2e-9f && eD <= 0.03f * dlo &&
+         eN * eN <= 0.99e-4f * r2lo * (dlo * dlo) &&
+         zl - near_z * dhi >= 3e-5f * (fabsf(g2.y) + near_z * dhi);
+}
+
+// Stage splat `id` of a step into lane slot `lane`: the decide record (AoS);
+// gv receives the GeomRec words (lin[0..11] in gv[0..2]). Returns the pixel
+// mask; `full` = the test box covers the whole block and every pixel of it is
+// surely live (tsb_block_surely_live), so the decide loop can skip the splat.
 __device__ __forceinline__ uint32_t tsb_stage_geom(const GeomRec* __restrict__ geom, int id,
                                                    int lane, int bx0, int by0, int bx1, int by1,
-                                                   DecRec* dec, float (*lin)[32]) {
+                                                   DecRec* dec, const BlockBox& bb, float near_z,
+                                                   bool& full, float4* gv) {
   const float4* gq = reinterpret_cast<const float4*>(geom + id);
-  const float4 gv[4] = {__ldg(gq), __ldg(gq + 1), __ldg(gq + 2), __ldg(gq + 3)};
+  gv[0] = __ldg(gq); gv[1] = __ldg(gq + 1); gv[2] = __ldg(gq + 2); gv[3] = __ldg(gq + 3);
   const uint32_t pm = tsb_block_pixmask(__float_as_uint(gv[3].x), __float_as_uint(gv[3].y), bx0,
                                         by0, bx1, by1);
+  full = pm == bb.valid && tsb_block_surely_live(gv[0], gv[1], gv[2], gv[3].w, bb, near_z);
   float4* d = reinterpret_cast<float4*>(dec + lane);
   d[0] = gv[0];
   d[1] = gv[1];
   d[2] = make_float4(gv[2].x, gv[2].y, gv[2].w, __uint_as_float(pm));
-  const float gl[11] = {gv[0].x, gv[0].y, gv[0].z, gv[0].w, gv[1].x, gv[1].y,
-                        gv[1].z, gv[1].w, gv[2].x, gv[2].y, gv[2].z};
-#pragma unroll
-  for (int c = 0; c < 11; ++c) lin[c][lane] = gl[c];
   return pm;
 }
 
