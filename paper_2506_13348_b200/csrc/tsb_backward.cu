@@ -423,11 +423,12 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
       const int cnt = hi - lo + 1;
       // ---- stage the step [lo, hi]
       __syncwarp();
-      bool hit = false, full = false;
+      bool hit = false;
+      uint32_t bflags = 0;
       if (lane < cnt) {
         const int id = __ldg(p.evals + lo + lane);
         float4 gv[4];
-        hit = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, bb, p.near_f, full,
+        hit = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, bb, p.near_f, bflags,
                              gv) != 0;
         const float gl[11] = {gv[0].x, gv[0].y, gv[0].z, gv[0].w, gv[1].x, gv[1].y,
                               gv[1].z, gv[1].w, gv[2].x, gv[2].y, gv[2].z};
@@ -446,7 +447,8 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
         for (int c = 0; c < 9; ++c) ws.mf[c][lane] = (float)__ldg(m64 + c);
       }
       const uint32_t cand = __ballot_sync(0xffffffffu, hit);
-      const uint32_t fullm = __ballot_sync(0xffffffffu, full);
+      const uint32_t fullm = __ballot_sync(0xffffffffu, (bflags & kBlockLive) != 0);
+      const uint32_t zsm = __ballot_sync(0xffffffffu, (bflags & kBlockZSafe) != 0);
       __syncwarp();
       if (!cand) continue;
       // ---- decide: this pixel's contributors in the step (entries <= last)
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
           for (int c = 0; c < 11; ++c) L[c] = ws.lin[c][k];
           L[11] = ws.dec[k].r2hi;
         };
-        live = (fullm | tsb_decide_step(ws.dec, load_lin, ws.sid, cand & ~fullm, lane, x, y,
+        live = (fullm | tsb_decide_step(ws.dec, load_lin, ws.sid, cand & ~fullm, zsm, lane, x, y,
                                         p.near_f, p.cam, p.m64, px, py)) & valid;
       }
       // ---- adjoint, back to front over the entries with a live pixel

@@ -63,11 +63,36 @@ __device__ __forceinline__ uint32_t tsb_block_pixmask(uint32_t gbx, uint32_t gby
 // result is exactly tsb_eval_lin + tsb_live_f64 of every candidate (tsb_math.h).
 template <class LoadLin>
 __device__ __forceinline__ uint32_t tsb_decide_step(const DecRec* dec, LoadLin load_lin,
-                                                    const int32_t* sid, uint32_t m, int lane,
-                                                    float x, float y, float near_f,
+                                                    const int32_t* sid, uint32_t m, uint32_t zs,
+                                                    int lane, float x, float y, float near_f,
                                                     const tsb_cam_params& cam, const double* m64,
                                                     int px, int py) {
   uint32_t live = 0, undecided = 0;
+  // z-safe candidates (kBlockZSafe): tsb_predecide_lin_nb reduces to the two
+  // q tests (|D| > eps and the depth test hold on the whole block)
+  for (uint32_t mz = m & zs; mz;) {
+    int kk[TSB_DECIDE_ILP];
+#pragma unroll
+    for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
+      kk[j] = mz ? __ffs(mz) - 1 : kk[0];
+      mz &= mz - 1;
+    }
+#pragma unroll
+    for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
+      const DecRec& g = dec[kk[j]];
+      const bool in = (g.pixmask >> lane) & 1u;
+      const float D = fmaf(g.lin[0], x, fmaf(g.lin[1], y, g.lin[2]));
+      const float Nu = fmaf(g.lin[3], x, fmaf(g.lin[4], y, g.lin[5]));
+      const float Nv = fmaf(g.lin[6], x, fmaf(g.lin[7], y, g.lin[8]));
+      const float q = fmaf(Nu, Nu, Nv * Nv);
+      const float D2 = D * D;
+      const bool sure = q <= tsb_lin_r2lo(g.r2hi) * D2;
+      const bool maybe = q <= g.r2hi * D2;
+      live |= (in && sure ? 1u : 0u) << kk[j];
+      undecided |= (in && maybe && !sure ? 1u : 0u) << kk[j];
+    }
+  }
+  m &= ~zs;
   while (m) {
     int kk[TSB_DECIDE_ILP];
 #pragma unroll
@@ -122,16 +147,20 @@ __device__ __forceinline__ BlockBox tsb_block_box(const tsb_cam_params& cam, int
   return b;
 }
 
-// Block-level "surely live": true only if tsb_predecide_lin_nb returns 1 (live)
-// at EVERY fp32 pixel point (x, y) of the block rectangle, so the warp can set
-// the splat's live bit for all its pixels without evaluating them. A
-// performance shortcut that never changes a decision. With S_F = |a|X+|b|Y+|c|
-// for a form F = a x + b y + c (X, Y = max |x|, |y| on the block):
+// Block-level facts about a splat, each true only if it holds at EVERY fp32
+// pixel point (x, y) of the block rectangle (performance shortcuts that never
+// change a decision):
+//   kBlockZSafe: |D~| > eps and the depth test of tsb_predecide_lin_nb passes
+//                (z surely > near), so the pixel's answer depends on q alone;
+//   kBlockLive:  additionally q <= r2lo D^2, i.e. the answer is 1 (live) — the
+//                warp sets the splat's live bit for all its pixels untested.
+// With S_F = |a|X+|b|Y+|c| for a form F = a x + b y + c (X, Y = max |x|, |y|):
 //  * e_F = 2^-21 S_F bounds the error of F's fp32 value at a pixel (two
 //    roundings: 2^-23 S_F) and at the corners, which are stepped from
 //    (x0, y0) by one or two more fmaf's with the rounded extents dx, dy.
 //  * D is affine: with every corner |D~| > eD of one sign, the exact D keeps
 //    that sign on the block and |D| >= dlo = min |D~_c| - eD there.
+//  * z: zs > zt holds with a 3e-5 relative margin at the largest pixel |D~|.
 //  * (x,y) -> (u,v) = (Nu/D, Nv/D) is projective without a pole on the block,
 //    so the block maps onto the convex quad of its corner images: the exact
 //    |(u,v)| on the block is at most its largest corner value rho.
@@ -139,11 +168,12 @@ __device__ __forceinline__ BlockBox tsb_block_box(const tsb_cam_params& cam, int
 //    (eN = e_Nu + e_Nv) give rho <= 0.9587 sqrt(r2lo); with eD <= 0.03 dlo the
 //    per-pixel fp32 N~ <= rho|D| + eN stays below 0.99999 sqrt(r2lo)(|D| - eD),
 //    so the pixel's own q <= r2lo D^2 (three roundings) holds; q <= r2hi D^2 too.
-//  * z: zs > zt holds with a 3e-5 relative margin at the largest pixel |D~|.
-// The GPU-vs-oracle bit-exact tests (tests/test_gpu_forward.py) check it.
-__device__ __forceinline__ bool tsb_block_surely_live(const float4& g0, const float4& g1,
-                                                      const float4& g2, float r2lo,
-                                                      const BlockBox& b, float near_z) {
+// The GPU-vs-oracle bit-exact tests (tests/test_gpu_forward.py) check both.
+constexpr uint32_t kBlockZSafe = 1u, kBlockLive = 2u;
+
+__device__ __forceinline__ uint32_t tsb_block_flags(const float4& g0, const float4& g1,
+                                                    const float4& g2, float r2lo,
+                                                    const BlockBox& b, float near_z) {
   // L0..L8 = D, Nu, Nv coefficients, L9 = det (tsb_make_lin)
   const float k21 = 4.76837158203125e-7f;  // 2^-21
   const float eD = k21 * fmaf(fabsf(g0.x), b.X, fmaf(fabsf(g0.y), b.Y, fabsf(g0.z)));
@@ -172,24 +202,26 @@ __device__ __forceinline__ bool tsb_block_surely_live(const float4& g0, const fl
   const float dlo = dmin - eD;
   const float dhi = dmax + 2.f * eD;
   const float zl = pos ? g2.y : -g2.y;
-  return (pos || neg) && in && dlo > 2e-9f && eD <= 0.03f * dlo &&
-         eN * eN <= 0.99e-4f * r2lo * (dlo * dlo) &&
-         zl - near_z * dhi >= 3e-5f * (fabsf(g2.y) + near_z * dhi);
+  const bool zsafe = (pos || neg) && dlo > 2e-9f && eD <= 0.03f * dlo &&
+                     zl - near_z * dhi >= 3e-5f * (fabsf(g2.y) + near_z * dhi);
+  const bool live = zsafe && in && eN * eN <= 0.99e-4f * r2lo * (dlo * dlo);
+  return (zsafe ? kBlockZSafe : 0u) | (live ? kBlockLive : 0u);
 }
 
 // Stage splat `id` of a step into lane slot `lane`: the decide record (AoS);
 // gv receives the GeomRec words (lin[0..11] in gv[0..2]). Returns the pixel
-// mask; `full` = the test box covers the whole block and every pixel of it is
-// surely live (tsb_block_surely_live), so the decide loop can skip the splat.
+// mask; `flags` = tsb_block_flags (kBlockLive only if the test box also covers
+// the whole block), so the decide loop can skip or simplify the splat.
 __device__ __forceinline__ uint32_t tsb_stage_geom(const GeomRec* __restrict__ geom, int id,
                                                    int lane, int bx0, int by0, int bx1, int by1,
                                                    DecRec* dec, const BlockBox& bb, float near_z,
-                                                   bool& full, float4* gv) {
+                                                   uint32_t& flags, float4* gv) {
   const float4* gq = reinterpret_cast<const float4*>(geom + id);
   gv[0] = __ldg(gq); gv[1] = __ldg(gq + 1); gv[2] = __ldg(gq + 2); gv[3] = __ldg(gq + 3);
   const uint32_t pm = tsb_block_pixmask(__float_as_uint(gv[3].x), __float_as_uint(gv[3].y), bx0,
                                         by0, bx1, by1);
-  full = pm == bb.valid && tsb_block_surely_live(gv[0], gv[1], gv[2], gv[3].w, bb, near_z);
+  flags = pm ? tsb_block_flags(gv[0], gv[1], gv[2], gv[3].w, bb, near_z) : 0u;
+  if (pm != bb.valid) flags &= ~kBlockLive;
   float4* d = reinterpret_cast<float4*>(dec + lane);
   d[0] = gv[0];
   d[1] = gv[1];
