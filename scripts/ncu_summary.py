@@ -57,11 +57,16 @@ def main(lpath, rpath, out):
     lines = ["# ncu summary", ""]
     ls = launches(lpath)
     # last frame: from the last k_preprocess to the end
+    # the last complete frame: a k_preprocess .. k_shade run of our kernels (the
+    # bench's own torch diagnostics between frames, at::*, are not frame work)
+    ls = [x for x in ls if not x[1].lstrip("void ").startswith("at::")]
     starts = [i for i, (_, n, _) in enumerate(ls) if "k_preprocess" in n]
-    frame = ls[starts[-1]:] if starts else ls
-    ends = [i for i, (_, n, _) in enumerate(frame) if "k_shade" in n]
-    if ends:
-        frame = frame[:ends[0] + 1]
+    frame = ls
+    for s in reversed(starts):
+        ends = [i for i, (_, n, _) in enumerate(ls[s:]) if "k_shade" in n]
+        if ends:
+            frame = ls[s:s + ends[0] + 1]
+            break
     tot = sum(t for _, _, t in frame)
     lines += ["## Launch list of one cfg2 frame (cold-cache, serialised; compare shares)", "",
               "| kernel | ns | share |", "|---|---:|---:|"]
