@@ -20,6 +20,7 @@
 // Reference: /root/reference/pkg/src/texsplat/rasterize.py:127-438,
 // shading.py:51-183 (see tsb_math.h for line-level citations).
 
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_fp16.h>
@@ -79,11 +80,7 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   cub::DeviceRadixSort::SortPairs(nullptr, b_tile, (const uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (const int32_t*)nullptr,
                                   (int32_t*)nullptr, (int)C, 0, bits);
-  size_t b_order = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b_order, (const uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (const int32_t*)nullptr,
-                                  (int32_t*)nullptr, L->num_tiles, 0, 16);
-  L->cub_bytes = std::max(std::max(b_depth, b_order), std::max(b_scan, b_tile));
+  L->cub_bytes = std::max(b_depth, std::max(b_scan, b_tile));
 
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
@@ -106,9 +103,6 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   L->evals_in = take(C * 4);
   L->evals_out = take(C * 4);
   L->ranges = take((size_t)L->num_tiles * 8);
-  L->tcost_in = take((size_t)L->num_tiles * 4);
-  L->tcost_out = take((size_t)L->num_tiles * 4);
-  L->torder_in = take((size_t)L->num_tiles * 4);
   L->torder_out = take((size_t)L->num_tiles * 4);
   L->counters = take(64);
   L->cub_tmp = take(L->cub_bytes);
@@ -734,20 +728,34 @@ k_raster_fwd(RasterParams p) {
   }
 }
 
-// Sort key for the persistent rasterizer's schedule: tiles by descending
-// list length (longest-processing-time first).
-__global__ void k_tile_cost(int32_t n, const int32_t* __restrict__ ranges,
-                            uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const int c = ranges[2 * t + 1] - ranges[2 * t];
-  keys[t] = 0xFFFFu - (uint32_t)(c < 0xFFFF ? c : 0xFFFF);
-  vals[t] = t;
+// The persistent rasterizer's schedule: tiles by descending list length
+// (longest-processing-time first). One CTA counting-sorts the tiles on
+// length/2 (clamped at 2047); the order inside a bucket is free — the
+// schedule never changes a result.
+constexpr int kSchedThreads = 1024;
+__global__ void __launch_bounds__(kSchedThreads) k_tile_schedule(int32_t nt,
+                                                                 const int32_t* __restrict__ ranges,
+                                                                 int32_t* __restrict__ order) {
+  using Scan = cub::BlockScan<int, kSchedThreads>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int cursor[kSchedThreads];
+  const int tid = threadIdx.x;
+  cursor[tid] = 0;
+  __syncthreads();
+  auto bucket = [&](int t) {
+    const int c = ranges[2 * t + 1] - ranges[2 * t];
+    return kSchedThreads - 1 - (min(c, 2 * kSchedThreads - 1) >> 1);
+  };
+  for (int t = tid; t < nt; t += kSchedThreads) atomicAdd(&cursor[bucket(t)], 1);
+  __syncthreads();
+  const int h = cursor[tid];
+  int start;
+  Scan(scan_tmp).ExclusiveSum(h, start);
+  cursor[tid] = start;
+  __syncthreads();
+  for (int t = tid; t < nt; t += kSchedThreads) order[atomicAdd(&cursor[bucket(t)], 1)] = t;
 }
 
-// ---------------------------------------------------------------------------
-// K6 shade
-// ---------------------------------------------------------------------------
 struct ShadeParams {
   tsb_cam_params cam;
   tsb_env_params env;
@@ -1033,20 +1041,10 @@ int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera, const
   rp.work_counter = reinterpret_cast<int32_t*>(ws_ptr<int64_t>(ws, L.counters) + 1);
   TSB_CUDA(cudaMemsetAsync(rp.work_counter, 0, 4, st));
   rp.tile_order = nullptr;
-#ifndef TSB_NO_TILE_ORDER
-  {
-    uint32_t* kin = ws_ptr<uint32_t>(ws, L.tcost_in);
-    int32_t* vin = ws_ptr<int32_t>(ws, L.torder_in);
-    k_tile_cost<<<(L.num_tiles + 255) / 256, 256, 0, st>>>(L.num_tiles, rp.ranges, kin, vin);
-    TSB_CHECK_LAUNCH("k_tile_cost");
-    size_t cb = L.cub_bytes;
-    TSB_CUDA(cub::DeviceRadixSort::SortPairs(ws_ptr<char>(ws, L.cub_tmp), cb, kin,
-                                             ws_ptr<uint32_t>(ws, L.tcost_out), vin,
-                                             ws_ptr<int32_t>(ws, L.torder_out), L.num_tiles, 0,
-                                             16, st));
-    rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);
-  }
-#endif
+  k_tile_schedule<<<1, kSchedThreads, 0, st>>>(L.num_tiles, rp.ranges,
+                                               ws_ptr<int32_t>(ws, L.torder_out));
+  TSB_CHECK_LAUNCH("k_tile_schedule");
+  rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);
   cudaError_t e;
   if (tile == 8) e = launch_raster<8>(mode, L.num_tiles, st, rp);
   else if (tile == 16) e = launch_raster<16>(mode, L.num_tiles, st, rp);

@@ -252,7 +252,7 @@ struct AtlasTex {
 struct WsLayout {
   size_t geom, rects, mat, m64, dkeys_in, dkeys_out, dk32_in, dk32_out, ids_in, ids_out, tile_count,
       counts_sorted, offsets, rank, ekeys_in, ekeys_out, evals_in, evals_out,
-      ranges, tcost_in, tcost_out, torder_in, torder_out, counters, cub_tmp;
+      ranges, torder_out, counters, cub_tmp;
   size_t cub_bytes;
   size_t total;
   int32_t tiles_x, tiles_y, num_tiles, tile_bits;
