@@ -141,43 +141,44 @@ class Renderer:
                      want_split=want_split, stream=stream)
         return col, gbuf
 
-    def stream_views(self, cameras, host_out=None):
+    def stream_views(self, cameras, host_out=None, depth: int = 2):
         """Render a sequence of views and read each colour image back to
-        pinned host memory, overlapping frame i's device->host copy with
-        frame i+1's render (double-buffered outputs, a dedicated copy stream).
-        Yields (index, host colour tensor) as each copy completes; the host
-        buffer is reused two frames later."""
+        pinned host memory, overlapping each frame's device->host copy with
+        the following renders (`depth` rotating output buffers, a dedicated
+        copy stream). Yields (index, host colour tensor) as each copy
+        completes; a host buffer is reused `depth` frames later."""
         cams = list(cameras)
         if not cams:
             return
         W, H = int(cams[0].width), int(cams[0].height)
         dev = self.device
-        key = ("stream", W, H)
+        key = ("stream", W, H, depth)
         if key not in self._bufs:  # pinned buffers, copy stream: allocated once
             self._bufs[key] = (
-                [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)],
-                [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True) for _ in range(2)],
+                [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(depth)],
+                [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True)
+                 for _ in range(depth)],
                 torch.cuda.Stream(dev))
         dcol, hcol_cached, copy = self._bufs[key]
         hcol = host_out or hcol_cached
         compute = torch.cuda.current_stream(dev)
-        done = [torch.cuda.Event(), torch.cuda.Event()]
-        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        done = [torch.cuda.Event() for _ in range(depth)]
+        ready = [torch.cuda.Event() for _ in range(depth)]
         for i, cam in enumerate(cams):
-            b = i & 1
-            if i >= 2:
+            b = i % depth
+            if i >= depth:
                 done[b].synchronize()           # host buffer b free again
-                yield i - 2, hcol[b]
-            compute.wait_event(done[b]) if i >= 2 else None  # device buffer b free
+                yield i - depth, hcol[b]
+                compute.wait_event(done[b])     # device buffer b free
             self.render(cam, check=False, stream=compute, color=dcol[b])
             ready[b].record(compute)
             copy.wait_event(ready[b])
             with torch.cuda.stream(copy):
                 hcol[b].copy_(dcol[b], non_blocking=True)
             done[b].record(copy)
-        for j in range(max(0, len(cams) - 2), len(cams)):
-            done[j & 1].synchronize()
-            yield j, hcol[j & 1]
+        for j in range(max(0, len(cams) - depth), len(cams)):
+            done[j % depth].synchronize()
+            yield j, hcol[j % depth]
 
     def shade(self, gbuf: GBuffer, camera) -> ShadeResult:
         c, d, s = shade_planar(gbuf.planar, camera, self.env, self.background)
