@@ -111,16 +111,25 @@ __device__ __forceinline__ EqTaps eq_taps(const tsb_grid& g, float dx, float dy,
 }
 
 // Adjoint of sample_equirect (environment.py:94-129): scatter `up` into the
-// grid gradient and return d/d(direction).
-__device__ void eq_grad(const tsb_grid& g, float* ggrid, float dx, float dy, float dz,
-                        const float* up, float* ddir) {
+// grid gradient and return d/d(direction). `rgba`: the gradient grid has 4
+// floats per texel (the sharded scratch) and each tap is one 16-byte vector
+// atomic instead of three scalar ones.
+__device__ void eq_grad(const tsb_grid& g, float* ggrid, bool rgba, float dx, float dy,
+                        float dz, const float* up, float* ddir) {
   const EqTaps t = eq_taps(g, dx, dy, dz);
   const float w00 = (1.0f - t.fc) * (1.0f - t.fr), w01 = t.fc * (1.0f - t.fr);
   const float w10 = (1.0f - t.fc) * t.fr, w11 = t.fc * t.fr;
+  if (ggrid && rgba) {
+    float4* g4 = reinterpret_cast<float4*>(ggrid);
+    atomicAdd(g4 + t.i00, make_float4(up[0] * w00, up[1] * w00, up[2] * w00, 0.f));
+    atomicAdd(g4 + t.i01, make_float4(up[0] * w01, up[1] * w01, up[2] * w01, 0.f));
+    atomicAdd(g4 + t.i10, make_float4(up[0] * w10, up[1] * w10, up[2] * w10, 0.f));
+    atomicAdd(g4 + t.i11, make_float4(up[0] * w11, up[1] * w11, up[2] * w11, 0.f));
+  }
   float dfc = 0.f, dfr = 0.f;
   for (int ch = 0; ch < 3; ++ch) {
     const float u = up[ch];
-    if (ggrid) {
+    if (ggrid && !rgba) {
       atomicAdd(ggrid + 3 * t.i00 + ch, u * w00);
       atomicAdd(ggrid + 3 * t.i01 + ch, u * w01);
       atomicAdd(ggrid + 3 * t.i10 + ch, u * w10);
@@ -149,6 +158,7 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
   if (pix >= W * H) return;
   // this CTA's private copy of the environment gradient grids
   const size_t shard = p.shard_stride ? (size_t)(blockIdx.x % kEnvShards) * p.shard_stride : 0;
+  const bool rgba = p.shard_stride != 0;  // shards hold 4 floats per texel
   const size_t HW = (size_t)W * H;
   float g[13];
 #pragma unroll
@@ -219,8 +229,8 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
       dmetal += df0 * (alb[c] - 0.04f);
     }
     float dn_diff[3];
-    eq_grad(env.diffuse, p.gdiffuse ? p.gdiffuse + shard : nullptr, n[0], n[1], n[2], dirr,
-            dn_diff);
+    eq_grad(env.diffuse, p.gdiffuse ? p.gdiffuse + shard : nullptr, rgba, n[0], n[1], n[2],
+            dirr, dn_diff);
     // LUT adjoint (environment.py:449-464)
     float dcos_cl, drough_lut;
     {
@@ -253,13 +263,13 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
       float up[3], dd[3];
       const float w0 = l1 != l0 ? 1.0f - fl : (1.0f - fl) + fl;
       for (int c = 0; c < 3; ++c) up[c] = dspec[c] * w0;
-      eq_grad(env.mips[l0], p.gmips[l0] ? p.gmips[l0] + shard : nullptr, wr[0], wr[1], wr[2],
-              up, dd);
+      eq_grad(env.mips[l0], p.gmips[l0] ? p.gmips[l0] + shard : nullptr, rgba, wr[0], wr[1],
+              wr[2], up, dd);
       for (int c = 0; c < 3; ++c) dwr[c] += dd[c];
       if (l1 != l0 && fl != 0.0f) {
         for (int c = 0; c < 3; ++c) up[c] = dspec[c] * fl;
-        eq_grad(env.mips[l1], p.gmips[l1] ? p.gmips[l1] + shard : nullptr, wr[0], wr[1],
-                wr[2], up, dd);
+        eq_grad(env.mips[l1], p.gmips[l1] ? p.gmips[l1] + shard : nullptr, rgba, wr[0],
+                wr[1], wr[2], up, dd);
         for (int c = 0; c < 3; ++c) dwr[c] += dd[c];
       }
     }
@@ -292,23 +302,27 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
   for (int c = 0; c < 13; ++c) p.dgbuf[c * HW + pix] = dg[c];
 }
 
-// Sum the environment-gradient shards into the caller's grids.
+// Sum the environment-gradient shards (4 floats per texel) into the caller's
+// (h, w, 3) grids.
 struct EnvShardPlan {
   float* dst[TSB_MAX_LEVELS + 1];   // caller grids: mips then diffuse
-  int32_t off[TSB_MAX_LEVELS + 2];  // float offset of each grid in a shard
+  int32_t off[TSB_MAX_LEVELS + 2];  // float offset of each grid in the caller layout (3/texel)
+  int32_t off4[TSB_MAX_LEVELS + 2]; // ... and in a shard (4/texel)
   int32_t nseg;
 };
 
-__global__ void k_env_shard_reduce(const float* __restrict__ shards, int32_t stride,
+__global__ void k_env_shard_reduce(const float* __restrict__ shards, int32_t n3, int32_t stride,
                                    EnvShardPlan plan) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= stride) return;
-  float s = 0.f;
-  for (int k = 0; k < kEnvShards; ++k) s += shards[(size_t)k * stride + i];
+  if (i >= n3) return;
   int seg = 0;
   while (seg + 1 < plan.nseg && plan.off[seg + 1] <= i) ++seg;
+  const int li = i - plan.off[seg];
+  const int j = plan.off4[seg] + 4 * (li / 3) + li % 3;
+  float s = 0.f;
+  for (int k = 0; k < kEnvShards; ++k) s += shards[(size_t)k * stride + j];
   float* d = plan.dst[seg];
-  if (d) d[i - plan.off[seg]] += s;
+  if (d) d[li] += s;
 }
 
 // ---------------------------------------------------------------------------
@@ -818,14 +832,15 @@ int tsb_backward_scratch_size(int32_t P, uint64_t* bytes) {
   return TSB_OK;
 }
 
-static int32_t env_floats(const tsb_environment* env, int32_t* off) {
+// Floats of all environment grids at `ch` floats per texel (offsets per grid).
+static int32_t env_floats(const tsb_environment* env, int32_t* off, int ch = 3) {
   int32_t o = 0;
   for (int l = 0; l < env->levels; ++l) {
     if (off) off[l] = o;
-    o += env->mip_h[l] * env->mip_w[l] * 3;
+    o += env->mip_h[l] * env->mip_w[l] * ch;
   }
   if (off) off[env->levels] = o;
-  o += env->diff_h * env->diff_w * 3;
+  o += env->diff_h * env->diff_w * ch;
   if (off) off[env->levels + 1] = o;
   return o;
 }
@@ -835,7 +850,7 @@ int tsb_shade_backward_scratch_size(const tsb_environment* env, uint64_t* bytes)
     set_error("tsb_shade_backward_scratch_size: invalid arguments");
     return TSB_ERR_VALUE;
   }
-  *bytes = (uint64_t)kEnvShards * env_floats(env, nullptr) * sizeof(float);
+  *bytes = (uint64_t)kEnvShards * env_floats(env, nullptr, 4) * sizeof(float);
   return TSB_OK;
 }
 
@@ -853,7 +868,8 @@ int tsb_shade_backward(const float* gbuf, const tsb_camera* camera, const tsb_en
   }
   cudaStream_t st = (cudaStream_t)stream;
   EnvShardPlan plan;
-  const int32_t nfl = env_floats(env, plan.off);
+  const int32_t nfl3 = env_floats(env, plan.off);
+  const int32_t nfl = env_floats(env, plan.off4, 4);
   const bool sharded = env_grads && scratch &&
                        scratch_bytes >= (uint64_t)kEnvShards * nfl * sizeof(float);
   ShadeBwdParams sp;
@@ -866,7 +882,7 @@ int tsb_shade_backward(const float* gbuf, const tsb_camera* camera, const tsb_en
     sp.env.mips[l].h = on ? env->mip_h[l] : 0;
     sp.env.mips[l].w = on ? env->mip_w[l] : 0;
     float* caller = (on && env_grads) ? env_grads->spec_mips[l] : nullptr;
-    sp.gmips[l] = sharded && caller ? sh + plan.off[l] : caller;
+    sp.gmips[l] = sharded && caller ? sh + plan.off4[l] : caller;
     plan.dst[l] = on ? caller : nullptr;
   }
   sp.env.diffuse.data = env->diffuse;
@@ -875,7 +891,7 @@ int tsb_shade_backward(const float* gbuf, const tsb_camera* camera, const tsb_en
   sp.env.lut = env->lut;
   sp.env.lut_res = env->lut_res;
   float* cdiff = env_grads ? env_grads->diffuse : nullptr;
-  sp.gdiffuse = sharded && cdiff ? sh + plan.off[env->levels] : cdiff;
+  sp.gdiffuse = sharded && cdiff ? sh + plan.off4[env->levels] : cdiff;
   plan.dst[env->levels] = cdiff;
   plan.nseg = env->levels + 1;
   sp.shard_stride = sharded ? nfl : 0;
@@ -886,7 +902,7 @@ int tsb_shade_backward(const float* gbuf, const tsb_camera* camera, const tsb_en
   k_shade_bwd<<<(n + 255) / 256, 256, 0, st>>>(sp);
   TSB_CHECK_LAUNCH("k_shade_bwd");
   if (sharded) {
-    k_env_shard_reduce<<<(nfl + 255) / 256, 256, 0, st>>>(sh, nfl, plan);
+    k_env_shard_reduce<<<(nfl3 + 255) / 256, 256, 0, st>>>(sh, nfl3, nfl, plan);
     TSB_CHECK_LAUNCH("k_env_shard_reduce");
   }
   return TSB_OK;
