@@ -165,6 +165,28 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   g.bx = (uint32_t)tb[0] | ((uint32_t)tb[1] << 16);
   g.by = (uint32_t)tb[2] | ((uint32_t)tb[3] << 16);
   g.id = id;
+  // Tile binning by the test box (reference rect ∩ alpha-cut ellipse box):
+  // a strictly tighter, conservative version of _tile_lists' rect binning
+  // (rasterize.py:246-258) — tiles outside it cannot hold a live pixel.
+  const bool binned = r.keep && tb[1] > tb[0] && tb[3] > tb[2];
+  p.tile_count[id] = binned ? tsb_rect_tile_count(tb[0], tb[1], tb[2], tb[3], p.tile) : 0;
+  // 24-bit sort key: (bits(z) - bits(near)) >> 32 is monotone in z for
+  // z > near (positive doubles order like their bit patterns; 2^-20
+  // relative resolution over 16 binades, farther depths clamp); equal keys
+  // are re-ordered by k_fix_runs on the full 64-bit pattern, so the result
+  // is the exact (z, id) order.
+  const uint64_t full = tsb_f64_bits(r.view_z);
+  p.dkeys[id] = r.keep ? full : ~0ull;
+  uint64_t k32 = kDepthCulled - 1;
+  if (r.keep) {
+    const uint64_t d = (full - p.near_bits) >> 32;
+    k32 = d < kDepthCulled - 1 ? d : kDepthCulled - 1;
+  }
+  p.dkey32[id] = r.keep ? (uint32_t)k32 : kDepthCulled;
+  p.ids[id] = id;
+  // the rasterizer and the backward read records only through tile-list
+  // entries: splats without entries (culled, or no pixel in the box) skip them
+  if (!binned) return;
   p.geom[id] = g;
 
   MatRec m;
@@ -185,64 +207,45 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   double* m64 = p.m64 + (size_t)kM64Stride * id;
   for (int k = 0; k < 9; ++k) m64[k] = r.m[k];
   m64[9] = op;
-
-  // 24-bit sort key: (bits(z) - bits(near)) >> 32 is monotone in z for
-  // z > near (positive doubles order like their bit patterns; 2^-20
-  // relative resolution over 16 binades, farther depths clamp); equal keys
-  // are re-ordered by k_fix_runs on the full 64-bit pattern, so the result
-  // is the exact (z, id) order.
-  const uint64_t full = tsb_f64_bits(r.view_z);
-  p.dkeys[id] = r.keep ? full : ~0ull;
-  uint64_t k32 = kDepthCulled - 1;
-  if (r.keep) {
-    const uint64_t d = (full - p.near_bits) >> 32;
-    k32 = d < kDepthCulled - 1 ? d : kDepthCulled - 1;
-  }
-  p.dkey32[id] = r.keep ? (uint32_t)k32 : kDepthCulled;
-  p.ids[id] = id;
-  // Tile binning by the test box (reference rect ∩ alpha-cut ellipse box):
-  // a strictly tighter, conservative version of _tile_lists' rect binning
-  // (rasterize.py:246-258) — tiles outside it cannot hold a live pixel.
-  const bool box_ok = tb[1] > tb[0] && tb[3] > tb[2];
-  p.tile_count[id] = (r.keep && box_ok) ? tsb_rect_tile_count(tb[0], tb[1], tb[2], tb[3], p.tile) : 0;
 }
 
-// S1b: runs of equal 32-bit depth keys leave the stable sort in id order;
-// sort each run by (full fp64 key, id) — runs are rare and short for real
-// scenes (one thread per run, insertion sort; already-sorted runs cost one
-// scan). The culled tail (key kDepthCulled) stays in id order.
-__global__ void k_fix_runs(int32_t P, const uint32_t* __restrict__ k32,
-                           const uint64_t* __restrict__ k64, int32_t* __restrict__ ids) {
+// S1b + K2: runs of equal 24-bit depth keys leave the stable sort in id
+// order; the thread at a run's start sorts the run by (full fp64 key, id) —
+// runs are rare and short for real scenes (insertion sort; already-sorted
+// runs cost one scan) — and then writes the tile count and rank of every
+// position of its run (singletons: their own). The culled tail (key
+// kDepthCulled) stays in id order.
+__global__ void k_fix_runs_rank(int32_t P, const uint32_t* __restrict__ k32,
+                                const uint64_t* __restrict__ k64, int32_t* __restrict__ ids,
+                                const int32_t* __restrict__ tile_count,
+                                int32_t* __restrict__ counts_sorted, int32_t* __restrict__ rank) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P - 1) return;
+  if (i >= P) return;
   const uint32_t k = k32[i];
-  if (k == kDepthCulled || k32[i + 1] != k || (i > 0 && k32[i - 1] == k)) return;
-  int end = i + 1;
-  while (end + 1 < P && k32[end + 1] == k) ++end;
-  for (int a = i + 1; a <= end; ++a) {
-    const int id = ids[a];
-    const uint64_t key = k64[id];
-    int b = a - 1;
-    while (b >= i) {
-      const int ob = ids[b];
-      const uint64_t kb = k64[ob];
-      if (kb < key || (kb == key && ob < id)) break;
-      ids[b + 1] = ob;
-      --b;
+  const bool fixable = k != kDepthCulled;
+  if (fixable && i > 0 && k32[i - 1] == k) return;  // inside a run: its start handles it
+  int end = i;
+  if (fixable) {
+    while (end + 1 < P && k32[end + 1] == k) ++end;
+    for (int a = i + 1; a <= end; ++a) {
+      const int id = ids[a];
+      const uint64_t key = k64[id];
+      int b = a - 1;
+      while (b >= i) {
+        const int ob = ids[b];
+        const uint64_t kb = k64[ob];
+        if (kb < key || (kb == key && ob < id)) break;
+        ids[b + 1] = ob;
+        --b;
+      }
+      ids[b + 1] = id;
     }
-    ids[b + 1] = id;
   }
-}
-
-// K2: per draw-order rank: tile count and rank of each id.
-__global__ void k_rank_counts(int32_t P, const int32_t* __restrict__ sorted_ids,
-                              const int32_t* __restrict__ tile_count,
-                              int32_t* __restrict__ counts_sorted, int32_t* __restrict__ rank) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P) return;
-  const int id = sorted_ids[r];
-  counts_sorted[r] = tile_count[id];
-  rank[id] = r;
+  for (int r = i; r <= end; ++r) {
+    const int id = ids[r];
+    counts_sorted[r] = tile_count[id];
+    rank[id] = r;
+  }
 }
 
 // K3 (load-balanced): one thread per 4 consecutive output entries. The
@@ -256,9 +259,26 @@ __global__ void __launch_bounds__(256) k_duplicate_lb(
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ counts_sorted,
     const int32_t* __restrict__ offsets, const GeomRec* __restrict__ boxes,
     uint32_t* __restrict__ ekeys, int32_t* __restrict__ evals, int64_t* __restrict__ counters) {
-  const int64_t e0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  __shared__ int s_lo, s_hi;
+  const int64_t eb = 4 * (int64_t)blockIdx.x * blockDim.x;
+  const int64_t e0 = eb + 4 * threadIdx.x;
   const int64_t total = (int64_t)offsets[P - 1] + counts_sorted[P - 1];
   if (blockIdx.x == 0 && threadIdx.x == 0) counters[0] = total;
+  // owner ranks of the block's first and last entries: every thread's
+  // binary search then runs over ~100 ranks (L1 hits) instead of all P
+  if (total <= cap && eb < total) {
+    auto owner = [&](int64_t e) {
+      int lo = 0, hi = P;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(offsets + mid) <= e) lo = mid; else hi = mid;
+      }
+      return lo;
+    };
+    if (threadIdx.x == 0) s_lo = owner(eb);
+    if (threadIdx.x == 32) s_hi = owner(min(eb + 4 * (int64_t)blockDim.x, total) - 1) + 1;
+    __syncthreads();
+  }
   if (e0 >= cap) return;
   if (total > cap || e0 >= total) {  // padding: sorts after every real tile
     if (e0 + 4 <= cap) {
@@ -268,8 +288,8 @@ __global__ void __launch_bounds__(256) k_duplicate_lb(
     }
     return;
   }
-  // upper_bound(offsets, e0) - 1
-  int lo = 0, hi = P;
+  // upper_bound(offsets, e0) - 1 within the block's owner range
+  int lo = s_lo, hi = s_hi;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (__ldg(offsets + mid) <= e0) lo = mid; else hi = mid;
@@ -982,11 +1002,9 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, ws_ptr<uint32_t>(ws, L.dk32_in),
                                              ws_ptr<uint32_t>(ws, L.dk32_out), ids_in, ids_out,
                                              P, 0, kDepthKeyBits, st));
-    k_fix_runs<<<(P + 255) / 256, 256, 0, st>>>(P, ws_ptr<uint32_t>(ws, L.dk32_out), dk_in,
-                                                ids_out);
-    TSB_CHECK_LAUNCH("k_fix_runs");
-    k_rank_counts<<<(P + 255) / 256, 256, 0, st>>>(P, ids_out, tcount, csorted, rank);
-    TSB_CHECK_LAUNCH("k_rank_counts");
+    k_fix_runs_rank<<<(P + 255) / 256, 256, 0, st>>>(P, ws_ptr<uint32_t>(ws, L.dk32_out), dk_in,
+                                                     ids_out, tcount, csorted, rank);
+    TSB_CHECK_LAUNCH("k_fix_runs_rank");
     cub_bytes = L.cub_bytes;
     TSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, csorted, offsets, P, st));
     const int64_t C = std::max<int64_t>(cap, 1);
