@@ -481,11 +481,12 @@ def main():
                         "colour into pinned host memory, host consumes each image; frame i's "
                         "copy overlaps frame i+1's render; camera passed by value in the "
                         "launch; scene, atlas, environment resident (uploaded once)"},
-        "gpu_launches": 8 * K,
+        "gpu_launches": 7 * K,
         "gpu_launches_note": "ours per frame (one CUDA graph replay per view): k_preprocess, "
-                             "k_fix_runs, k_rank_counts, k_duplicate_lb, k_ranges, k_tile_cost, "
-                             "k_raster_fwd, k_shade (+ CUB radix sort/scan kernels in the same "
-                             "graph)",
+                             "k_fix_runs_rank, k_duplicate_lb, k_ranges, k_tile_schedule, "
+                             "k_raster_fwd, k_shade; the same graph also holds 11 CUB kernels "
+                             "(depth and tile radix sorts, the tile-count scan) launched by "
+                             "libtsb.so",
     }
     if world == 1 and not args.no_cpu_baseline:
         fps, cores, sample, _ = cpu_baseline_run(args, args.cpu_frames)
