@@ -601,10 +601,12 @@ k_raster_fwd(RasterParams p) {
                                            p.near_f, bflags, gv);
         hit = pm != 0;
         ws.sid[lane] = id;
-        const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
-        float4* rec = ws.rec[lane];
-        rec[0] = gv[0]; rec[1] = gv[1]; rec[2] = gv[2];
-        rec[4] = __ldg(mq); rec[5] = __ldg(mq + 1); rec[6] = __ldg(mq + 2); rec[3] = __ldg(mq + 3);
+        if (hit) {  // the material record only for splats touching the block
+          const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
+          float4* rec = ws.rec[lane];
+          rec[0] = gv[0]; rec[1] = gv[1]; rec[2] = gv[2];
+          rec[4] = __ldg(mq); rec[5] = __ldg(mq + 1); rec[6] = __ldg(mq + 2); rec[3] = __ldg(mq + 3);
+        }
       }
       const uint32_t cand = __ballot_sync(0xffffffffu, hit);
       const uint32_t fullm = __ballot_sync(0xffffffffu, (bflags & kBlockLive) != 0);

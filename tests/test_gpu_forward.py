@@ -332,3 +332,26 @@ def test_frame_graph_matches_launches_and_rejects_other_sizes():
         _lib.check(_lib.lib().tsb_frame_graph_launch(h, C.byref(_lib.camera_struct(other)), None,
                                                      None), "graph")
     r.close()
+
+
+def test_full_hd_tile8_many_tiles_bit_exact():
+    """1920x1080 at 8-px tiles (32,400 tiles: the one-CTA tile schedule loops,
+    several hundred blocks per raster launch) and a camera close enough that
+    splats cross the near plane and fill blocks whole (z-safe / surely-live
+    block tests on both sides): structure and verify-mode pixels bit-exact."""
+    scene = synth.make_shell_scene(6000, 4, seed=11)
+    cam = synth.bench_cameras(8, 1920, 1080)[3]
+    gbuf, tape = render_forward(scene, cam, "perprim", tile=8, with_tape=True)
+    ref = oracle.render(scene, cam, tile=8)
+    _assert_structure_equal(tape, ref)
+    _assert_pixels_equal(gbuf, ref)
+    assert np.array_equal(_np(gbuf.planar), ref["gbuf"])
+    # inside-out close-up: the eye 0.12 from the shell, splats near the eye
+    # reach behind the near plane (full-screen rects, not z-safe blocks)
+    near = Camera.look_at((0.0, 0.0, 1.12), (0.0, 0.0, 0.0), fov_x_deg=100.0, width=320,
+                          height=240, near=0.05)
+    gbuf, tape = render_forward(scene, near, "perprim", tile=16, with_tape=True)
+    ref = oracle.render(scene, near, tile=16)
+    _assert_structure_equal(tape, ref)
+    _assert_pixels_equal(gbuf, ref)
+    assert np.array_equal(_np(gbuf.planar), ref["gbuf"])
