@@ -432,11 +432,13 @@ def main():
     n_touched = int(touched.sum(dtype=torch.int64).item())
     entries = r.entries_needed()
     alg_bytes = 68 * W * H + 4 * entries + 128 * P + 2 * n_touched * T * T * texel_b
-    traffic = None
+    traffic, ncu_l1 = None, None
     tj = ROOT / "profiles" / "traffic.json"
     if tj.exists():
-        tv = _json.loads(tj.read_text()).get(f"{args.config}/{args.sampler}/{args.texel_format}")
-        traffic = tv
+        tjd = _json.loads(tj.read_text())
+        traffic = tjd.get(f"{args.config}/{args.sampler}/{args.texel_format}")
+        if f"{args.config}/{args.sampler}/{args.texel_format}" == "cfg2/hw/rgba32f":
+            ncu_l1 = tjd.get("ncu")
     hbm_achieved = alg_bytes / rast_avg_s / 1e9
     fetch_rate = 2 * fragments / rast_avg_s / 1e9 if args.sampler != "flat" else 0.0
 
@@ -473,7 +475,8 @@ def main():
                          "frac": round(fetch_rate / tex_peak, 4) if tex_peak else None,
                          "peak_source": "measured live: tsb_tex_probe bilinear RGBA fetches, "
                                         "L1-resident 32x32 window of the same texture",
-                         "fetches_per_launch": 2 * fragments},
+                         "fetches_per_launch": 2 * fragments,
+                         "ncu_l1tex": ncu_l1},
         "clocks": clk,
         "e2e": {"value": round(e2e_fps, 3), "unit": "frames/s",
                 "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": H * W * 3 * 4,

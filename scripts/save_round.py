@@ -31,9 +31,11 @@ shutil.copy(src / "launches.csv", dst / f"{tag}_launches.csv")
 subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_summary.py"), str(src / "launches.csv"),
                 str(src / "full.ncu-rep"), str(dst / f"{tag}_ncu_summary.md")], check=True,
                stdout=subprocess.DEVNULL)
-raw = subprocess.run(["ncu", "-i", str(src / "full.ncu-rep"), "--page", "raw", "--csv", "--metrics",
-                      "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True,
-                     text=True).stdout
+M = ("dram__bytes_read.sum,dram__bytes_write.sum,l1tex__throughput.avg.pct_of_peak_sustained_active,"
+     "dram__cycles_active.avg.pct_of_peak_sustained_elapsed,"
+     "l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed")
+raw = subprocess.run(["ncu", "-i", str(src / "full.ncu-rep"), "--page", "raw", "--csv", "--metrics", M],
+                     capture_output=True, text=True).stdout
 rows = list(csv.DictReader(io.StringIO(raw)))
 for r in rows[1:]:
     if "k_raster_fwd" in r["Kernel Name"]:
@@ -41,6 +43,11 @@ for r in rows[1:]:
         unit_r, unit_w = rows[0]["dram__bytes_read.sum"], rows[0]["dram__bytes_write.sum"]
         tb = (float(r["dram__bytes_read.sum"]) * mult[unit_r] +
               float(r["dram__bytes_write.sum"]) * mult[unit_w])
-        (dst / "traffic.json").write_text(json.dumps({"cfg2/hw/rgba32f": int(tb)}) + "\n")
-        print("k_raster_fwd DRAM bytes per launch", int(tb))
+        out = {"cfg2/hw/rgba32f": int(tb),
+               "ncu": {"kernel": "k_raster_fwd (cfg2, hw, rgba32f)",
+                       "l1tex_throughput_pct": float(r["l1tex__throughput.avg.pct_of_peak_sustained_active"]),
+                       "tex_data_pipe_pct": float(r["l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed"]),
+                       "dram_throughput_pct": float(r["dram__cycles_active.avg.pct_of_peak_sustained_elapsed"])}}
+        (dst / "traffic.json").write_text(json.dumps(out) + "\n")
+        print("k_raster_fwd", out)
         break
