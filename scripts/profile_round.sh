@@ -14,6 +14,8 @@ if [ "${1:-}" != "quick" ]; then
   done; done
   run hw16f python bench.py --texel-format rgba16f --steps 100 --warmup 10 --no-cpu-baseline
 fi
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/train_launches.csv \
+  python scripts/profile_train.py 3 > $O/ncu_train.log 2>&1; echo "ncu train list rc=$?"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 3 > $O/ncu_list.log 2>&1; echo "ncu list rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_raster_fwd|k_preprocess|k_shade" -s 10 -c 3 \

@@ -28,6 +28,8 @@ for f in sorted(src.glob("*.json")):
 if table3:
     (dst / f"{tag}_table3.json").write_text(json.dumps(table3, indent=1) + "\n")
 shutil.copy(src / "launches.csv", dst / f"{tag}_launches.csv")
+if (src / "train_launches.csv").exists():
+    shutil.copy(src / "train_launches.csv", dst / f"{tag}_train_launches.csv")
 subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_summary.py"), str(src / "launches.csv"),
                 str(src / "full.ncu-rep"), str(dst / f"{tag}_ncu_summary.md")], check=True,
                stdout=subprocess.DEVNULL)
