@@ -405,9 +405,6 @@ __device__ __forceinline__ void tsb_decode_normal_approx(float ea, float eb, con
 #ifndef TSB_PAIR_ILP
 #define TSB_PAIR_ILP 2
 #endif
-#ifndef TSB_PAIR_PIPE
-#define TSB_PAIR_PIPE 0
-#endif
 
 #ifdef TSB_STATS
 // Work counters of k_raster_fwd (instrumented builds only: make EXTRA=-DTSB_STATS):
@@ -639,60 +636,6 @@ k_raster_fwd(RasterParams p) {
         }
       }
 #endif
-#if TSB_PAIR_PIPE
-      // ---- texture + blend, in order, software-pipelined per lane: the fetches
-      // of the next TSB_PAIR_ILP live pairs are in flight while the current ones
-      // blend (the texture latency is the kernel's top stall otherwise)
-      {
-        int kc[TSB_PAIR_ILP];
-        bool hc[TSB_PAIR_ILP];
-        PairFetch fc[TSB_PAIR_ILP];
-#pragma unroll
-        for (int j = 0; j < TSB_PAIR_ILP; ++j) {
-          hc[j] = live != 0;
-          kc[j] = hc[j] ? __ffs(live) - 1 : 0;
-          live &= live - 1;
-          if (hc[j]) pair_issue<MODE>(p, ws, kc[j], make_float2(x, y), fc[j]);
-        }
-        while (__any_sync(0xffffffffu, hc[0])) {
-          int kn[TSB_PAIR_ILP];
-          bool hn[TSB_PAIR_ILP];
-          PairFetch fn[TSB_PAIR_ILP];
-#pragma unroll
-          for (int j = 0; j < TSB_PAIR_ILP; ++j) {
-            hn[j] = live != 0;
-            kn[j] = hn[j] ? __ffs(live) - 1 : 0;
-            live &= live - 1;
-            if (hn[j]) pair_issue<MODE>(p, ws, kn[j], make_float2(x, y), fn[j]);
-          }
-#pragma unroll
-          for (int j = 0; j < TSB_PAIR_ILP; ++j) {
-            if (hc[j] && !done) {
-              const int k = kc[j];
-              float rv[13];
-              pair_result<MODE>(ws, fc[j], rv);
-              float xa[12];
-#pragma unroll
-              for (int c = 0; c < 8; ++c) xa[c] = rv[c];
-              xa[8] = rv[10]; xa[9] = rv[11]; xa[10] = rv[12];
-              xa[11] = rv[8];
-              T_last = T;
-              T = tsb_composite(acc, xa, rv[9], T);
-              ++n;
-              last = base + k;
-              if (p.touched) p.touched[ws.sid[k]] = 1;
-              if (!(T > teps)) { done = true; live = 0; }
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < TSB_PAIR_ILP; ++j) {
-            hc[j] = hn[j] && !done;
-            kc[j] = kn[j];
-            fc[j] = fn[j];
-          }
-        }
-      }
-#else
       // ---- texture + blend, in order, TSB_PAIR_ILP live pairs per lane per iteration
       while (__any_sync(0xffffffffu, live != 0)) {
 #ifdef TSB_STATS
@@ -733,7 +676,6 @@ k_raster_fwd(RasterParams p) {
           }
         }
       }
-#endif
       __syncwarp();
     }
     if (inside) {
