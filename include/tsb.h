@@ -155,6 +155,17 @@ int tsb_frame_graph_create(const tsb_scene* scene, const tsb_camera* camera,
                            float* gbuf, const tsb_pixel_state* pixels, int64_t* entries_needed,
                            const tsb_environment* env, const float* background, float* color,
                            float* diffuse, float* specular, tsb_frame_graph_t* graph);
+/* As tsb_frame_graph_create, with a caller-owned cudaEvent_t recorded by
+ * every replay between binning and rasterisation (may be NULL): a copy
+ * stream waiting on it overlaps the previous frame's read-back with this
+ * frame's rasteriser instead of its latency-bound binning. */
+int tsb_frame_graph_create_ev(const tsb_scene* scene, const tsb_camera* camera,
+                              const tsb_atlas* atlas, int32_t mode, int32_t tile,
+                              void* workspace, uint64_t workspace_bytes, int64_t max_entries,
+                              float* gbuf, const tsb_pixel_state* pixels,
+                              int64_t* entries_needed, const tsb_environment* env,
+                              const float* background, float* color, float* diffuse,
+                              float* specular, void* binned_event, tsb_frame_graph_t* graph);
 int tsb_frame_graph_launch(tsb_frame_graph_t graph, const tsb_camera* camera, float* color,
                            void* stream);
 int tsb_frame_graph_destroy(tsb_frame_graph_t graph);

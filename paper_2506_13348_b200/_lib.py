@@ -123,6 +123,10 @@ _SIGNATURES = {
                                C.c_int32, C.c_int32, _P, C.c_uint64, C.c_int64, _P,
                                C.POINTER(PixelState_t), _P, C.POINTER(Environment_t), _P, _P,
                                _P, _P, C.POINTER(C.c_void_p)],
+    "tsb_frame_graph_create_ev": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
+                                  C.c_int32, C.c_int32, _P, C.c_uint64, C.c_int64, _P,
+                                  C.POINTER(PixelState_t), _P, C.POINTER(Environment_t), _P, _P,
+                                  _P, _P, _P, C.POINTER(C.c_void_p)],
     "tsb_frame_graph_launch": [_P, C.POINTER(Camera_t), _P, _P],
     "tsb_frame_graph_destroy": [_P],
     "tsb_env_scratch_size": [C.c_int32, C.c_int32, C.POINTER(C.c_uint64)],

@@ -1242,6 +1242,18 @@ int tsb_frame_graph_create(const tsb_scene* scene, const tsb_camera* camera, con
                            float* gbuf, const tsb_pixel_state* px, int64_t* entries_needed,
                            const tsb_environment* env, const float* background, float* color,
                            float* diffuse, float* specular, tsb_frame_graph_t* out) {
+  return tsb_frame_graph_create_ev(scene, camera, atlas, mode, tile, ws, ws_bytes, cap, gbuf, px,
+                                   entries_needed, env, background, color, diffuse, specular,
+                                   nullptr, out);
+}
+
+int tsb_frame_graph_create_ev(const tsb_scene* scene, const tsb_camera* camera,
+                              const tsb_atlas* atlas, int32_t mode, int32_t tile, void* ws,
+                              uint64_t ws_bytes, int64_t cap, float* gbuf,
+                              const tsb_pixel_state* px, int64_t* entries_needed,
+                              const tsb_environment* env, const float* background, float* color,
+                              float* diffuse, float* specular, void* binned_event,
+                              tsb_frame_graph_t* out) {
   if (!out || !camera) {
     set_error("tsb_frame_graph_create: null argument");
     return TSB_ERR_VALUE;
@@ -1269,8 +1281,16 @@ int tsb_frame_graph_create(const tsb_scene* scene, const tsb_camera* camera, con
   if (e != cudaSuccess) { delete g; return cuda_fail("cudaStreamCreate", e); }
   e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
   if (e == cudaSuccess) {
-    rc = tsb_render_forward(scene, camera, atlas, mode, tile, ws, ws_bytes, cap, gbuf, px,
-                            entries_needed, s);
+    rc = tsb_render_binning(scene, camera, atlas, mode, tile, ws, ws_bytes, cap, entries_needed,
+                            s);
+    if (rc == TSB_OK && binned_event) {  // an event-record node between binning and raster
+      // (external: a real event-record node, not a capture-internal fork marker)
+      const cudaError_t er =
+          cudaEventRecordWithFlags((cudaEvent_t)binned_event, s, cudaEventRecordExternal);
+      if (er != cudaSuccess) rc = cuda_fail("cudaEventRecord", er);
+    }
+    if (rc == TSB_OK)
+      rc = tsb_render_composite(scene, camera, atlas, mode, tile, ws, ws_bytes, cap, gbuf, px, s);
     if (rc == TSB_OK && env)
       rc = tsb_shade_forward(gbuf, camera, env, background, color, diffuse, specular, s);
     cudaGraph_t graph = nullptr;

@@ -73,18 +73,20 @@ class Renderer:
     def entries_needed(self) -> int:
         return int(self.prep.workspace.needed.item())
 
-    def _graph(self, camera, W, H):
+    def _graph(self, camera, W, H, binned_event=None):
         """CUDA graph of this view size over the current buffers (rebuilt if
-        the workspace was reallocated)."""
+        the workspace was reallocated). `binned_event`: a torch.cuda.Event the
+        graph records between binning and rasterisation on every replay."""
         ws = self.prep.workspace
         gb, px, col, _, _ = self._buffers(W, H)
-        key = (_lib.ptr(ws.buf), ws.capacity, ws.nbytes)
-        cur = self._graphs.get((W, H))
+        ev = None if binned_event is None else binned_event.cuda_event
+        key = (_lib.ptr(ws.buf), ws.capacity, ws.nbytes, ev)
+        cur = self._graphs.get((W, H, ev))
         if cur is not None and cur[0] == key:
             return cur[1], col
         if cur is not None:
             _lib.lib().tsb_frame_graph_destroy(cur[1])
-            del self._graphs[(W, H)]
+            del self._graphs[(W, H, ev)]
         L = _lib.lib()
         sc, at, cam = self.prep.scene.struct(), self.prep.atlas.struct(), _lib.camera_struct(camera)
         pst = px.struct()
@@ -93,12 +95,12 @@ class Renderer:
                                [float(v) for v in np.asarray(self.background, np.float64)]))
         from .rasterize import _MODES
         h = C.c_void_p()
-        _lib.check(L.tsb_frame_graph_create(
+        _lib.check(L.tsb_frame_graph_create_ev(
             C.byref(sc), C.byref(cam), C.byref(at), _MODES[self.prep.sampler], self.tile,
             _lib.ptr(ws.buf), ws.nbytes, ws.capacity, _lib.ptr(gb), C.byref(pst),
-            _lib.ptr(ws.needed), C.byref(env), bg, _lib.ptr(col), None, None, C.byref(h)),
-            "tsb_frame_graph_create")
-        self._graphs[(W, H)] = (key, h)
+            _lib.ptr(ws.needed), C.byref(env), bg, _lib.ptr(col), None, None,
+            C.c_void_p(ev) if ev else None, C.byref(h)), "tsb_frame_graph_create_ev")
+        self._graphs[(W, H, ev)] = (key, h)
         return h, col
 
     def close(self):
@@ -112,18 +114,22 @@ class Renderer:
         except Exception:  # noqa: BLE001 — interpreter shutdown
             pass
 
+    def _graph_ready(self, W, H) -> bool:
+        ws = self.prep.workspace
+        return (self.use_graph and ws.buf is not None
+                and ws.key == (self.prep.scene.num_splats, W, H, self.tile))
+
     def render(self, camera, *, check: bool = True, want_split: bool = False, stream=None,
-               color=None):
+               color=None, binned_event=None):
         """Forward + shade one view. Returns (color (H,W,3), GBuffer), both on
         the GPU; buffers are reused across calls of the same size (pass
         `color` to shade into a caller-owned buffer instead). With
         check=False (workspace already reserved) the view replays a CUDA
-        graph of the whole frame (tsb_frame_graph_*)."""
+        graph of the whole frame (tsb_frame_graph_*), which records
+        `binned_event` (if given) once the frame's tile lists are built."""
         W, H = int(camera.width), int(camera.height)
-        ws = self.prep.workspace
-        if (not check and not want_split and self.use_graph and ws.buf is not None
-                and ws.key == (self.prep.scene.num_splats, W, H, self.tile)):
-            h, col = self._graph(camera, W, H)
+        if not check and not want_split and self._graph_ready(W, H):
+            h, col = self._graph(camera, W, H, binned_event)
             out = color if color is not None else col
             cam = _lib.camera_struct(camera)
             _lib.check(_lib.lib().tsb_frame_graph_launch(h, C.byref(cam), _lib.ptr(out),
@@ -143,40 +149,60 @@ class Renderer:
 
     def stream_views(self, cameras, host_out=None, depth: int = 2):
         """Render a sequence of views and read each colour image back to
-        pinned host memory, overlapping each frame's device->host copy with
-        the following renders (`depth` rotating output buffers, a dedicated
-        copy stream). Yields (index, host colour tensor) as each copy
+        pinned host memory (`depth` rotating output buffers, a dedicated copy
+        stream). Frame i's device->host copy starts once frame i+1's tile
+        lists are built (an event recorded inside the frame graph), so it
+        overlaps frame i+1's rasteriser rather than its latency-bound
+        binning. Yields (index, host colour tensor) in order as each copy
         completes; a host buffer is reused `depth` frames later."""
         cams = list(cameras)
         if not cams:
             return
         W, H = int(cams[0].width), int(cams[0].height)
         dev = self.device
+        depth = max(2, int(depth))
         key = ("stream", W, H, depth)
-        if key not in self._bufs:  # pinned buffers, copy stream: allocated once
+        if key not in self._bufs:  # pinned buffers, copy stream, events: allocated once
+            binned = torch.cuda.Event()
+            binned.record()  # materialise the CUDA event before it is captured
             self._bufs[key] = (
                 [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(depth)],
                 [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True)
                  for _ in range(depth)],
-                torch.cuda.Stream(dev))
-        dcol, hcol_cached, copy = self._bufs[key]
+                torch.cuda.Stream(dev), binned)
+        dcol, hcol_cached, copy, binned = self._bufs[key]
         hcol = host_out or hcol_cached
         compute = torch.cuda.current_stream(dev)
         done = [torch.cuda.Event() for _ in range(depth)]
-        ready = [torch.cuda.Event() for _ in range(depth)]
-        for i, cam in enumerate(cams):
-            b = i % depth
-            if i >= depth:
-                done[b].synchronize()           # host buffer b free again
-                yield i - depth, hcol[b]
-                compute.wait_event(done[b])     # device buffer b free
-            self.render(cam, check=False, stream=compute, color=dcol[b])
-            ready[b].record(compute)
-            copy.wait_event(ready[b])
+        ready = torch.cuda.Event()
+        use_ev = self._graph_ready(W, H)
+
+        def queue_copy(j, after):
+            b = j % depth
+            copy.wait_event(after)
             with torch.cuda.stream(copy):
                 hcol[b].copy_(dcol[b], non_blocking=True)
             done[b].record(copy)
-        for j in range(max(0, len(cams) - depth), len(cams)):
+
+        for i, cam in enumerate(cams):
+            b = i % depth
+            if i >= depth:
+                compute.wait_event(done[b])     # device buffer b copied out
+            self.render(cam, check=False, stream=compute, color=dcol[b],
+                        binned_event=binned if use_ev else None)
+            if i >= 1:
+                if use_ev:
+                    queue_copy(i - 1, binned)   # frame i-1 done, frame i binned
+                else:
+                    ready.record(compute)       # no graph: after frame i
+                    queue_copy(i - 1, ready)
+            if i >= 2:
+                done[(i - 2) % depth].synchronize()
+                yield i - 2, hcol[(i - 2) % depth]
+        n = len(cams)
+        ready.record(compute)
+        queue_copy(n - 1, ready)
+        for j in range(max(0, n - 2), n):
             done[j % depth].synchronize()
             yield j, hcol[j % depth]
 

@@ -355,3 +355,26 @@ def test_full_hd_tile8_many_tiles_bit_exact():
     _assert_structure_equal(tape, ref)
     _assert_pixels_equal(gbuf, ref)
     assert np.array_equal(_np(gbuf.planar), ref["gbuf"])
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_stream_views_yields_each_frame_in_order(use_graph):
+    """Renderer.stream_views (the e2e path: read-back of frame i overlapped
+    with frame i+1, started from an event inside the frame graph) returns
+    every view's colour image, in order, identical to a plain render."""
+    from paper_2506_13348_b200.environment import BrdfLut
+    scene = synth.make_shell_scene(3000, 4, seed=5, with_environment=True)
+    cams = synth.bench_cameras(7, 160, 120)
+    r = Renderer(scene, pack_atlases(scene), scene.environment, BrdfLut.build(32, 128))
+    need = 0
+    for c in cams:
+        r.render(c)
+        need = max(need, r.entries_needed())
+    r.reserve(cams[0], need + 1024)
+    r.use_graph = use_graph
+    expect = [_np(r.render(c)[0]).copy() for c in cams]
+    for n in (1, 2, 5, 7):
+        got = [(i, img.numpy().copy()) for i, img in r.stream_views(cams[:n])]
+        assert [i for i, _ in got] == list(range(n))
+        for i, img in got:
+            assert np.array_equal(img, expect[i]), (n, i)
