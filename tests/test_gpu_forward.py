@@ -378,3 +378,19 @@ def test_stream_views_yields_each_frame_in_order(use_graph):
         assert [i for i, _ in got] == list(range(n))
         for i, img in got:
             assert np.array_equal(img, expect[i]), (n, i)
+
+
+def test_render_normal_and_depth_maps():
+    """reference test_rasterize.py:150-161 (fp32 tolerances)."""
+    from paper_2506_13348_b200.rasterize import render_depth_map, render_normal_map
+    scene = _facing_scene([0.0], [0.9], [(0.3, 0.3, 0.3)])
+    scene.scales[:] = 0.05  # tiny footprint so the corners stay uncovered
+    cam = _center_camera()
+    gb = render_forward(scene, cam)
+    assert float(gb.alpha[0, 0]) == 0.0
+    n = _np(render_normal_map(scene, cam))
+    assert np.allclose(n[16, 16], [0.5, 0.5, 1.0], atol=1e-6)
+    assert np.allclose(n[0, 0], 0.5)  # uncovered -> mid-gray
+    d = _np(render_depth_map(scene, cam))
+    assert abs(float(d[16, 16]) - 2.0) < 1e-5
+    assert float(d[0, 0]) == 0.0
