@@ -71,7 +71,7 @@ __device__ __forceinline__ void block_sums_atomic(double (&v)[K], double* dst) {
   }
 }
 
-constexpr int kRowsPerBlock = 8;
+constexpr int kRowsPerBlock = 2;
 
 // ---- K10 pass 1: display images, L1 / MSE sums, horizontal blur of the
 // five SSIM moments (a, b, a^2, b^2, ab) per channel -> m5[15][H][W].
@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(256) k_ssim_pass2(int W, int H, const float* _
   const int x = x0 + tx;
   const size_t HW = (size_t)W * H;
   double msum[1] = {0.0};
-  for (int c = 0; c < 3; ++c) {
-    __syncthreads();
+  {
+    const int c = blockIdx.z;  // one colour channel per CTA layer
     stage_vtile<5>(tile, m5 + (size_t)(5 * c) * HW, HW, W, H, x0, y0);
     __syncthreads();
     for (int r = ty; r < kTY; r += 8) {
@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(256) k_ssim_pass4(int W, int H, const float* _
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int x = x0 + tx;
   const size_t HW = (size_t)W * H;
-  for (int c = 0; c < 3; ++c) {
-    __syncthreads();
+  {
+    const int c = blockIdx.z;  // one colour channel per CTA layer
     stage_vtile<3>(tile, hb + (size_t)(3 * c) * HW, HW, W, H, x0, y0);
     __syncthreads();
     for (int r = ty; r < kTY; r += 8) {
@@ -644,7 +644,7 @@ int tsb_loss_image(const float* color, const float* target, int32_t width, int32
   const dim3 strips((width + 255) / 256, (height + kRowsPerBlock - 1) / kRowsPerBlock);
   k_ssim_pass1<<<strips, 256, 0, st>>>(width, height, color, target, m5, terms);
   TSB_CHECK_LAUNCH("k_ssim_pass1");
-  const dim3 vtiles((width + kTX - 1) / kTX, (height + kTY - 1) / kTY);
+  const dim3 vtiles((width + kTX - 1) / kTX, (height + kTY - 1) / kTY, 3);
   k_ssim_pass2<<<vtiles, 256, 0, st>>>(width, height, m5, part,
                                      (float)(-0.5 * dssim_weight / N), terms);
   TSB_CHECK_LAUNCH("k_ssim_pass2");
