@@ -175,8 +175,15 @@ def run_reference(args):
         "steps": min(frames, 5), "warmup": 1, "ms_per_step": round(1e3 / fps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD, "splats": args.splats, "texture_res": args.texture_res,
-                   "width": args.width, "height": args.height},
+        "config": {"workload": WORKLOAD if args.config == "cfg2" else
+                   f"{args.config}: {args.splats} textured 2D Gaussians, {args.texture_res}x"
+                   f"{args.texture_res} atlas, {args.width}x{args.height}",
+                   "splats": args.splats, "texture_res": args.texture_res,
+                   "width": args.width, "height": args.height,
+                   "sampler": "fp32 bilinear (the reference's lerp_corners arithmetic)",
+                   "texel_format": "rgba32f", "tile": args.tile,
+                   "views": "bench_cameras(256) orbit, views 0.. in order",
+                   "parallelism": f"{cores} host threads (OpenMP over tiles), rank 0 only"},
         "cpu_baseline": {"value": round(fps, 6), "unit": "frames/s", "cores": cores,
                          "kind": "port", "sample": sample, "note": CPU_BASELINE_NOTE},
         "e2e": {"value": round(fps, 6), "unit": "frames/s", "h2d_bytes_per_step": 0,
