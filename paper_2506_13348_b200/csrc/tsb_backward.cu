@@ -476,7 +476,11 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
           for (int c = 0; c < 11; ++c) L[c] = ws.lin[c][k];
           L[11] = ws.dec[k].r2hi;
         };
-        live = (fullm | tsb_decide_step(ws.dec, load_lin, ws.sid, cand & ~fullm, zsm, lane, x, y,
+        auto dec_at = [&](int k) {
+          const DecRec& d = ws.dec[k];
+          return DecRef{d.lin, d.r2hi, d.pixmask};
+        };
+        live = (fullm | tsb_decide_step(dec_at, load_lin, ws.sid, cand & ~fullm, zsm, lane, x, y,
                                         p.near_f, p.cam, p.m64, px, py)) & valid;
       }
       // ---- adjoint, back to front over the entries with a live pixel

@@ -405,6 +405,9 @@ __device__ __forceinline__ void tsb_decode_normal_approx(float ea, float eb, con
 #ifndef TSB_PAIR_ILP
 #define TSB_PAIR_ILP 2
 #endif
+#ifndef TSB_RASTER_CARVEOUT
+#define TSB_RASTER_CARVEOUT 44  // percent of 228 KB: 100 KB for 3 x 31 KB CTAs
+#endif
 
 #ifdef TSB_STATS
 // Work counters of k_raster_fwd (instrumented builds only: make EXTRA=-DTSB_STATS):
@@ -415,12 +418,14 @@ __device__ unsigned long long g_tsb_stats[16];
 
 // Warp-private shared memory of the rasterizer.
 struct WarpSmem {
-  // staged step, AoS for the decide loop (all lanes read the same splat)
-  DecRec dec[32];
   int32_t sid[32];            // splat ids
-  // the same step for texturing / blending, one 112-byte record per entry
-  // read with 128-bit loads (7 x 16 B: the stride is odd in 16-byte units, so
-  // lanes reading different entries of one quarter-warp rarely share banks):
+  uint32_t pm[32];            // the entry's pixel mask of the current block
+  // one 112-byte record per entry, read with 128-bit loads (7 x 16 B: the
+  // stride is odd in 16-byte units, so lanes reading different entries of one
+  // quarter-warp rarely share banks); the decide loop reads [0..2] with every
+  // lane on the same entry (broadcast), texturing reads all of it. One copy
+  // per warp keeps the CTA at <= 33 KB of shared memory, so 3 CTAs/SM fit the
+  // 100 KB carveout and L1 keeps ~156 KB for the atlas:
   //   [0] L0..L3  [1] L4..L7  [2] L8, det, opacity, r2hi   (intersection forms)
   //   [3] chart origin x, y (texels), page, linear offset
   //   [4] frame 0..3  [5] frame 4..7  [6] frame 8, clamped SH radiance rgb
@@ -594,10 +599,11 @@ k_raster_fwd(RasterParams p) {
       if (e < end) {
         const int id = __ldg(p.evals + e);
         float4 gv[4];
-        const uint32_t pm = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, bb,
+        const uint32_t pm = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, nullptr, bb,
                                            p.near_f, bflags, gv);
         hit = pm != 0;
         ws.sid[lane] = id;
+        ws.pm[lane] = pm;
         if (hit) {  // the material record only for splats touching the block
           const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
           float4* rec = ws.rec[lane];
@@ -614,7 +620,10 @@ k_raster_fwd(RasterParams p) {
       uint32_t live = 0;
       if (!done)
         live = fullm | tsb_decide_step(
-                           ws.dec,
+                           [&](int k) {
+                             const float* l = reinterpret_cast<const float*>(ws.rec[k]);
+                             return DecRef{l, l[11], ws.pm[k]};
+                           },
                            [&](int k, float* L) {
                              const float4 a = ws.rec[k][0], b = ws.rec[k][1], c = ws.rec[k][2];
                              L[0] = a.x; L[1] = a.y; L[2] = a.z; L[3] = a.w;
@@ -807,6 +816,11 @@ inline cudaError_t launch_raster_mode(int blocks, cudaStream_t st, const RasterP
   if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(k_raster_fwd<TILE, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // the smallest shared-memory carveout that holds the resident CTAs: the
+    // rest of the 256 KB stays L1, which caches the atlas texels
+    e = cudaFuncSetAttribute(k_raster_fwd<TILE, MODE>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, TSB_RASTER_CARVEOUT);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;

@@ -61,8 +61,16 @@ __device__ __forceinline__ uint32_t tsb_block_pixmask(uint32_t gbx, uint32_t gby
 // guard band for the rare undecided pairs. `load_lin(k, L)` fills L[0..11]
 // (tsb_make_lin's words) of staged entry k, `sid` holds the splat ids. The
 // result is exactly tsb_eval_lin + tsb_live_f64 of every candidate (tsb_math.h).
-template <class LoadLin>
-__device__ __forceinline__ uint32_t tsb_decide_step(const DecRec* dec, LoadLin load_lin,
+// What the decide loop reads of staged entry k: the linear forms L0..L9
+// (+ opacity, r2hi), the α-cut reject bound r2hi and the block pixel mask.
+struct DecRef {
+  const float* lin;
+  float r2hi;
+  uint32_t pixmask;
+};
+
+template <class DecAt, class LoadLin>
+__device__ __forceinline__ uint32_t tsb_decide_step(DecAt dec_at, LoadLin load_lin,
                                                     const int32_t* sid, uint32_t m, uint32_t zs,
                                                     int lane, float x, float y, float near_f,
                                                     const tsb_cam_params& cam, const double* m64,
@@ -79,7 +87,7 @@ __device__ __forceinline__ uint32_t tsb_decide_step(const DecRec* dec, LoadLin l
     }
 #pragma unroll
     for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
-      const DecRec& g = dec[kk[j]];
+      const DecRef g = dec_at(kk[j]);
       const bool in = (g.pixmask >> lane) & 1u;
       const float D = fmaf(g.lin[0], x, fmaf(g.lin[1], y, g.lin[2]));
       const float Nu = fmaf(g.lin[3], x, fmaf(g.lin[4], y, g.lin[5]));
@@ -102,7 +110,7 @@ __device__ __forceinline__ uint32_t tsb_decide_step(const DecRec* dec, LoadLin l
     }
 #pragma unroll
     for (int j = 0; j < TSB_DECIDE_ILP; ++j) {
-      const DecRec& g = dec[kk[j]];
+      const DecRef g = dec_at(kk[j]);
       const bool in = (g.pixmask >> lane) & 1u;
       const int r = tsb_predecide_lin_nb(g.lin, g.r2hi, x, y, near_f);
       live |= (in && r == 1 ? 1u : 0u) << kk[j];
@@ -222,10 +230,12 @@ __device__ __forceinline__ uint32_t tsb_stage_geom(const GeomRec* __restrict__ g
                                         by0, bx1, by1);
   flags = pm ? tsb_block_flags(gv[0], gv[1], gv[2], gv[3].w, bb, near_z) : 0u;
   if (pm != bb.valid) flags &= ~kBlockLive;
-  float4* d = reinterpret_cast<float4*>(dec + lane);
-  d[0] = gv[0];
-  d[1] = gv[1];
-  d[2] = make_float4(gv[2].x, gv[2].y, gv[2].w, __uint_as_float(pm));
+  if (dec) {  // (the forward reads the forms from its own record instead)
+    float4* d = reinterpret_cast<float4*>(dec + lane);
+    d[0] = gv[0];
+    d[1] = gv[1];
+    d[2] = make_float4(gv[2].x, gv[2].y, gv[2].w, __uint_as_float(pm));
+  }
   return pm;
 }
 
