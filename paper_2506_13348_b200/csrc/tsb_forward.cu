@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= p.P) return;
   const int K = (p.sh_degree + 1) * (p.sh_degree + 1);
-  double pos[3], tu[3], tv[3], s[2], sh[48];
+  double pos[3], tu[3], tv[3], s[2];
   for (int j = 0; j < 3; ++j) {
     pos[j] = p.pos[3 * id + j];
     tu[j] = p.tu[3 * id + j];
@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   }
   s[0] = p.sc[2 * id];
   s[1] = p.sc[2 * id + 1];
-  for (int k = 0; k < 3 * K; ++k) sh[k] = p.sh[(size_t)3 * K * id + k];
+  // SH coefficients read in place (a local copy would live in local memory)
+  const double* sh = p.sh + (size_t)3 * K * id;
   tsb_prep r;
   tsb_preprocess_splat(&p.cam, pos, tu, tv, s, sh, p.sh_degree, &r);
   const double op = p.op[id];
