@@ -60,6 +60,10 @@ typedef struct tsb_scene {
   const double* scales;        /* P x 2 */
   const double* opacities;     /* P     */
   const double* sh;            /* P x K x 3 */
+  const int32_t* record_slot;  /* P or NULL: where each splat's per-frame records
+                                  live in the workspace (a storage permutation for
+                                  locality, e.g. Morton order of position; it never
+                                  changes a result). NULL = identity */
 } tsb_scene;
 
 typedef struct tsb_atlas_tex* tsb_atlas_tex_t;

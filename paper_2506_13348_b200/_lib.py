@@ -40,7 +40,7 @@ class Scene_t(C.Structure):
     _fields_ = [("num_splats", C.c_int32), ("sh_degree", C.c_int32),
                 ("positions", C.c_void_p), ("tangent_u", C.c_void_p),
                 ("tangent_v", C.c_void_p), ("scales", C.c_void_p),
-                ("opacities", C.c_void_p), ("sh", C.c_void_p)]
+                ("opacities", C.c_void_p), ("sh", C.c_void_p), ("record_slot", C.c_void_p)]
 
 
 class Atlas_t(C.Structure):

@@ -440,16 +440,17 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
       bool hit = false;
       uint32_t bflags = 0;
       if (lane < cnt) {
-        const int id = __ldg(p.evals + lo + lane);
+        const int rs = __ldg(p.evals + lo + lane);  // the entry's record slot
         float4 gv[4];
-        hit = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, ws.dec, bb, p.near_f, bflags,
+        hit = tsb_stage_geom(p.geom, rs, lane, bx0, by0, bx1, by1, ws.dec, bb, p.near_f, bflags,
                              gv) != 0;
+        const int id = __float_as_int(gv[3].z);  // splat id (GeomRec.id)
         const float gl[11] = {gv[0].x, gv[0].y, gv[0].z, gv[0].w, gv[1].x, gv[1].y,
                               gv[1].z, gv[1].w, gv[2].x, gv[2].y, gv[2].z};
 #pragma unroll
         for (int c = 0; c < 11; ++c) ws.lin[c][lane] = gl[c];
         ws.sid[lane] = id;
-        const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
+        const float4* mq = reinterpret_cast<const float4*>(p.mat + rs);
         const float4 m0 = __ldg(mq), m1 = __ldg(mq + 1), m2 = __ldg(mq + 2), m3 = __ldg(mq + 3);
         ws.frame[0][lane] = m0.x; ws.frame[1][lane] = m0.y; ws.frame[2][lane] = m0.z;
         ws.frame[3][lane] = m0.w; ws.frame[4][lane] = m1.x; ws.frame[5][lane] = m1.y;

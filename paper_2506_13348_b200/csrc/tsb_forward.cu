@@ -134,6 +134,7 @@ struct PrepParams {
   uint64_t near_bits;
   int32_t* ids;
   int32_t* tile_count;
+  const int32_t* slot;  // record storage permutation (tsb_scene.record_slot) or null
 };
 
 #ifndef TSB_PREP_MINB
@@ -189,7 +190,8 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   // the rasterizer and the backward read records only through tile-list
   // entries: splats without entries (culled, or no pixel in the box) skip them
   if (!binned) return;
-  p.geom[id] = g;
+  const int sl = p.slot ? p.slot[id] : id;  // records live at the splat's slot
+  p.geom[sl] = g;
 
   MatRec m;
   for (int k = 0; k < 9; ++k) m.frame[k] = (float)r.frame[k];
@@ -204,9 +206,9 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   } else {
     m.tex_x = m.tex_y = 0.f; m.page = 0; m.lin_off = 0;
   }
-  p.mat[id] = m;
+  p.mat[sl] = m;
 
-  double* m64 = p.m64 + (size_t)kM64Stride * id;
+  double* m64 = p.m64 + (size_t)kM64Stride * id;  // the rare fp64 recheck: by id
   for (int k = 0; k < 9; ++k) m64[k] = r.m[k];
   m64[9] = op;
 }
@@ -260,7 +262,8 @@ __global__ void __launch_bounds__(256) k_duplicate_lb(
     int32_t P, int32_t tile, int32_t tiles_x, int64_t cap,
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ counts_sorted,
     const int32_t* __restrict__ offsets, const GeomRec* __restrict__ boxes,
-    uint32_t* __restrict__ ekeys, int32_t* __restrict__ evals, int64_t* __restrict__ counters) {
+    const int32_t* __restrict__ slot, uint32_t* __restrict__ ekeys, int32_t* __restrict__ evals,
+    int64_t* __restrict__ counters) {
   __shared__ int s_lo, s_hi;
   const int64_t eb = 4 * (int64_t)blockIdx.x * blockDim.x;
   const int64_t e0 = eb + 4 * threadIdx.x;
@@ -313,6 +316,7 @@ __global__ void __launch_bounds__(256) k_duplicate_lb(
       cur = r;
       off = __ldg(offsets + r);
       id = __ldg(sorted_ids + r);
+      if (slot) id = __ldg(slot + id);  // entries name the record slot
       const uint32_t bx = __ldg(&boxes[id].bx), by = __ldg(&boxes[id].by);
       const int x0 = bx & 0xFFFF, x1 = bx >> 16, y0 = by & 0xFFFF;
       tx0 = x0 / tile;
@@ -612,17 +616,17 @@ k_raster_fwd(RasterParams p) {
       uint32_t bflags = 0;
       __syncwarp();
       if (e < end) {
-        const int id = __ldg(p.evals + e);
+        const int rs = __ldg(p.evals + e);  // the entry's record slot
         float4 gv[4];
         DecRec* dcopy = nullptr;
         if constexpr (SEP) dcopy = ws.dec;
-        const uint32_t pm = tsb_stage_geom(p.geom, id, lane, bx0, by0, bx1, by1, dcopy, bb,
+        const uint32_t pm = tsb_stage_geom(p.geom, rs, lane, bx0, by0, bx1, by1, dcopy, bb,
                                            p.near_f, bflags, gv);
         hit = pm != 0;
-        ws.sid[lane] = id;
+        ws.sid[lane] = __float_as_int(gv[3].z);  // splat id (GeomRec.id)
         ws.pm[lane] = pm;
         if (hit) {  // the material record only for splats touching the block
-          const float4* mq = reinterpret_cast<const float4*>(p.mat + id);
+          const float4* mq = reinterpret_cast<const float4*>(p.mat + rs);
           float4* rec = ws.rec[lane];
           rec[0] = gv[0]; rec[1] = gv[1]; rec[2] = gv[2];
           rec[4] = __ldg(mq); rec[5] = __ldg(mq + 1); rec[6] = __ldg(mq + 2); rec[3] = __ldg(mq + 3);
@@ -785,13 +789,15 @@ __global__ void __launch_bounds__(256) k_shade(ShadeParams p) {
 // Export + atlas textures + TEX probe
 // ---------------------------------------------------------------------------
 __global__ void k_export_keys(int64_t cap, const uint32_t* __restrict__ ekeys,
-                              const int32_t* __restrict__ evals, const int32_t* __restrict__ rank,
+                              const int32_t* __restrict__ evals, const GeomRec* __restrict__ geom,
+                              const int32_t* __restrict__ rank,
                               const int64_t* __restrict__ counters, int64_t* __restrict__ keys) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cap) return;
   int64_t total = counters[0];
   if (total > cap) total = 0;
-  keys[i] = i < total ? (((int64_t)ekeys[i] << 32) | (int64_t)(uint32_t)rank[evals[i]]) : -1;
+  keys[i] = i < total ? (((int64_t)ekeys[i] << 32) | (int64_t)(uint32_t)rank[geom[evals[i]].id])
+                      : -1;  // entries name record slots; the record carries the id
 }
 
 __global__ void k_export_rects(int32_t P, const uint2* __restrict__ rc, int32_t* __restrict__ rects) {
@@ -977,6 +983,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     pp.dkey32 = ws_ptr<uint32_t>(ws, L.dk32_in);
     pp.near_bits = tsb_f64_bits(camera->near_z);
     pp.tile_count = tcount;
+    pp.slot = scene->record_slot;
     k_preprocess<<<(P + 255) / 256, 256, 0, st>>>(pp);
     TSB_CHECK_LAUNCH("k_preprocess");
 
@@ -990,7 +997,8 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     TSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, csorted, offsets, P, st));
     const int64_t C = std::max<int64_t>(cap, 1);
     k_duplicate_lb<<<(unsigned)((C + 1023) / 1024), 256, 0, st>>>(
-        P, tile, L.tiles_x, cap, ids_out, csorted, offsets, geom, ek_in, ev_in, counters);
+        P, tile, L.tiles_x, cap, ids_out, csorted, offsets, geom, scene->record_slot, ek_in, ev_in,
+        counters);
     TSB_CHECK_LAUNCH("k_duplicate_lb");
     cub_bytes = L.cub_bytes;
     TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, ek_in, ek_out, ev_in, ev_out,
@@ -1085,7 +1093,8 @@ int tsb_frame_export(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap,
   if (keys && cap > 0) {
     k_export_keys<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(
         cap, ws_ptr<uint32_t>(ws, L.ekeys_out), ws_ptr<int32_t>(ws, L.evals_out),
-        ws_ptr<int32_t>(ws, L.rank), ws_ptr<int64_t>(ws, L.counters), keys);
+        ws_ptr<GeomRec>(ws, L.geom), ws_ptr<int32_t>(ws, L.rank), ws_ptr<int64_t>(ws, L.counters),
+        keys);
     TSB_CHECK_LAUNCH("k_export_keys");
   }
   if (rects && P > 0) {

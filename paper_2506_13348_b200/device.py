@@ -31,6 +31,20 @@ def _dev(device):
     return torch.device(device)
 
 
+def morton_order(positions: np.ndarray, bits: int = 10) -> np.ndarray:
+    """Splat indices sorted by the Morton (Z-order) code of their positions."""
+    p = np.asarray(positions, np.float64)
+    if len(p) == 0:
+        return np.zeros(0, np.int64)
+    lo, ext = p.min(0), max(float(np.ptp(p, axis=0).max()), 1e-300)
+    q = np.clip(((p - lo) / ext * ((1 << bits) - 1)).astype(np.int64), 0, (1 << bits) - 1)
+    code = np.zeros(len(q), np.int64)
+    for b in range(bits):
+        for a in range(3):
+            code |= ((q[:, a] >> b) & 1) << (3 * b + a)
+    return np.argsort(code, kind="stable")
+
+
 class DeviceScene:
     """Splat parameters resident in HBM (float64, the reference's dtype)."""
 
@@ -55,6 +69,14 @@ class DeviceScene:
         self.opacities = up(scene.opacities, (P,))
         self.sh = up(scene.sh, (P, K, 3))
         self.texture_resolution = int(scene.texture_config.resolution)
+        # per-frame records stored in Morton order of position: splats that
+        # share a tile sit close in memory when the rasteriser stages them
+        self.record_slot = None
+        if P > 1:
+            order = morton_order(scene.positions)
+            slot = np.empty(P, np.int32)
+            slot[order] = np.arange(P, dtype=np.int32)
+            self.record_slot = torch.from_numpy(slot).to(dev)
 
     @staticmethod
     def from_tensors(positions, tangent_u, tangent_v, scales, opacities, sh, sh_degree,
@@ -66,6 +88,7 @@ class DeviceScene:
         self.positions, self.tangent_u, self.tangent_v = positions, tangent_u, tangent_v
         self.scales, self.opacities, self.sh = scales, opacities, sh
         self.texture_resolution = int(texture_resolution)
+        self.record_slot = None
         return self
 
     def struct(self) -> _lib.Scene_t:
@@ -78,6 +101,7 @@ class DeviceScene:
         s.scales = _lib.ptr(self.scales)
         s.opacities = _lib.ptr(self.opacities)
         s.sh = _lib.ptr(self.sh)
+        s.record_slot = _lib.ptr(getattr(self, "record_slot", None))
         return s
 
 

@@ -90,7 +90,7 @@ def test_error_mapping():
 
 def test_ctypes_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.Camera_t) == 16 * 8 + 6 * 8 + 8
-    assert ctypes.sizeof(_lib.Scene_t) == 8 + 6 * 8
+    assert ctypes.sizeof(_lib.Scene_t) == 8 + 7 * 8
     assert ctypes.sizeof(_lib.Atlas_t) == 16 + 5 * 8 + 8
     assert ctypes.sizeof(_lib.PixelState_t) == 5 * 8
 
