@@ -489,8 +489,10 @@ def main():
                 "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": H * W * 3 * 4,
                 "note": "Renderer.stream_views: render + D2H of every frame's (H,W,3) float32 "
                         "colour into pinned host memory, host consumes each image; frame i's "
-                        "copy overlaps frame i+1's render; camera passed by value in the "
-                        "launch; scene, atlas, environment resident (uploaded once)"},
+                        "copy starts from an event recorded inside frame i+1's graph after its "
+                        "binning, so it runs under frame i+1's rasteriser; camera passed by "
+                        "value in the launch; scene, atlas, environment resident (uploaded "
+                        "once)"},
         "gpu_launches": 7 * K,
         "gpu_launches_note": "ours per frame (one CUDA graph replay per view): k_preprocess, "
                              "k_fix_runs_rank, k_duplicate_lb, k_ranges, k_tile_schedule, "
