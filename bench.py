@@ -260,10 +260,17 @@ def main():
     from paper_2506_13348_b200.shading import shade_planar
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # (TSB_BENCH_DEVICE / TSB_BENCH_BACKEND: test hooks that run every rank on
+    # one GPU over gloo to exercise the multi-rank code path on a 1-GPU box)
+    gpu = int(os.environ.get("TSB_BENCH_DEVICE", local))
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("TSB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     scene = synth.make_shell_scene(args.splats, args.texture_res, seed=3, with_environment=True,
                                    env_height=args.env_height)
@@ -345,7 +352,7 @@ def main():
     for i in range(args.warmup):
         _lib.check(L.tsb_frame_graph_launch(graph, C.byref(cams_c[i % len(cams_c)]),
                                             _lib.ptr(col), sh), "graph")
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     clocks.start()
     if world > 1:
         dist.barrier()
