@@ -123,15 +123,20 @@ class DeviceAtlas:
         ind = atlas_set.indirection
         ind.validate()
         self.resolution = int(atlas_set.resolution)
-        pa = np.stack([p.texels for p in atlas_set.family_a]).astype(np.float32, copy=False)
-        pb = np.stack([p.texels for p in atlas_set.family_b]).astype(np.float32, copy=False)
-        self.pages, self.page_h, self.page_w = int(pa.shape[0]), int(pa.shape[1]), int(pa.shape[2])
+        p0 = atlas_set.family_a[0].texels
+        self.pages, self.page_h, self.page_w = len(atlas_set.family_a), int(p0.shape[0]), int(p0.shape[1])
         if self.pages * self.page_h * self.page_w >= 2 ** 31:
             raise ValueError("atlas larger than 2^31 texels per family")
         self.entries = torch.from_numpy(np.ascontiguousarray(ind.entries, np.int32)).to(dev)
         self.num_entries = int(ind.entries.shape[0])
-        fa = torch.from_numpy(np.ascontiguousarray(pa)).to(dev)
-        fb = torch.from_numpy(np.ascontiguousarray(pb)).to(dev)
+        # page by page into one device tensor per family (no host-side stack:
+        # a cfg5 atlas is 2 x 8.3 GB)
+        shape = (self.pages, self.page_h, self.page_w, 4)
+        fa = torch.empty(shape, dtype=torch.float32, device=dev)
+        fb = torch.empty(shape, dtype=torch.float32, device=dev)
+        for i, (qa, qb) in enumerate(zip(atlas_set.family_a, atlas_set.family_b)):
+            fa[i].copy_(torch.from_numpy(np.ascontiguousarray(qa.texels, np.float32)))
+            fb[i].copy_(torch.from_numpy(np.ascontiguousarray(qb.texels, np.float32)))
         self.family_a = fa if linear else None
         self.family_b = fb if linear else None
         self.texel_format = texel_format

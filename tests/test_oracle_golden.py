@@ -91,7 +91,7 @@ def test_cfg2_full_frame():
     K = r["num_kept"]
     assert np.array_equal(r["sorted_ids"][:K], g["order"])
     diff = r["n_contrib"] != g["counts"]
-    assert diff.sum() <= 64, diff.sum()
+    assert diff.sum() <= 15, diff.sum()  # observed: 15 gate flips
     assert np.abs(r["gbuf"][12] - g["alpha"]).max() <= TOL
     color, _, _ = oracle.shade(r["gbuf"], cam, scene.environment, gio.load("lut")["table"],
                                scene.background)
@@ -116,3 +116,56 @@ def test_box_binning_is_conservative(case):
     assert len(b["keys"]) <= len(a["keys"])
     for k in ("gbuf", "n_contrib", "final_T", "T_last"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def _gate_flips_only(ours, ref):
+    """Contributor counts equal the reference's except T > 1e-4 gate flips
+    (fp32 vs fp64 transmittance): each differs by one fragment, and at most
+    one pixel in 2000 flips (observed: 15 / 640,000 on the full cfg2 frame)."""
+    d = np.asarray(ours, np.int64) - np.asarray(ref, np.int64)
+    assert np.abs(d).max() <= 1
+    assert int((d != 0).sum()) <= max(2, d.size // 2000), int((d != 0).sum())
+
+
+def _crop_case(g, pre, scene, lut_table, env):
+    """Oracle vs a reference crop window (tests/golden/make_golden_scale.py):
+    counts exact except T-gate flips, all 13 G-buffer channels and the
+    colour within the north_star bar."""
+    cam = gio.camera(g, pre + "cam_")
+    r = oracle.render(scene, cam)
+    K = r["num_kept"]
+    assert np.array_equal(r["sorted_ids"][:K], g[pre + "order"])
+    _gate_flips_only(r["n_contrib"], g[pre + "counts"])
+    ref = g[pre + "gbuf"].transpose(2, 0, 1)
+    for c in range(13):
+        assert np.abs(r["gbuf"][c] - ref[c]).max() <= TOL, c
+    color, _, _ = oracle.shade(r["gbuf"], cam, env, lut_table, scene.background)
+    assert np.abs(color - g[pre + "color"]).max() <= TOL
+    return r
+
+
+def _check_sha(g, scene):
+    import hashlib
+    for k in ("positions", "tangent_u", "scales", "texels"):
+        h = hashlib.sha256(np.ascontiguousarray(getattr(scene, k)).tobytes()).hexdigest()
+        assert h == str(g["sha_" + k]), k
+
+
+def test_cfg2_full_frame_gbuffer_windows(lut_table):
+    """All 13 G-buffer channels of the full cfg2 frame on three 160x160
+    windows (centre, two silhouette windows)."""
+    g = gio.load("cfg2_gbuf")
+    scene = gio.cfg2_scene()
+    _check_sha(g, scene)
+    for pre in ("c_", "s_", "e_"):
+        _crop_case(g, pre, scene, lut_table, scene.environment)
+
+
+def test_cfg3_crop_two_page_shape(lut_table):
+    """cfg3 geometry: 500k splats, T=8 (a 2-page atlas), 1920x1080 view 37
+    of the 256-view orbit, 128x128 silhouette crop."""
+    from paper_2506_13348_b200 import synth
+    g = gio.load("cfg3_crop")
+    scene = synth.make_shell_scene(500_000, 8, seed=3, with_environment=True)
+    _check_sha(g, scene)
+    _crop_case(g, "", scene, lut_table, scene.environment)
