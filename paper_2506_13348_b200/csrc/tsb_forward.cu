@@ -638,6 +638,23 @@ k_raster_fwd(RasterParams p) {
       __syncwarp();
       if (!cand) continue;
       // ---- decide (splats surely live on the whole block need no per-pixel test)
+      // z-safe candidates: each lane tests its own splat at all 32 pixels
+      // (tsb_decide_candidate), then a bit transpose gives each pixel lane its
+      // live / undecided candidates; the rest go through the per-pixel loop.
+      uint32_t lc = 0, uc = 0;
+      const bool zc = hit && (bflags & (kBlockZSafe | kBlockLive)) == kBlockZSafe;
+      if (__any_sync(0xffffffffu, zc)) {
+        float xs[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) xs[c] = __shfl_sync(0xffffffffu, x, c);
+        // (the staged forms of this lane's own entry; written for every hit)
+        lc = tsb_decide_candidate(ws.rec[lane][0], ws.rec[lane][1], ws.rec[lane][2], xs, y, uc);
+        const uint32_t keep = zc ? ws.pm[lane] : 0u;
+        lc &= keep;
+        uc &= keep;
+        lc = tsb_warp_transpose32(lc, lane);
+        uc = tsb_warp_transpose32(uc, lane);
+      }
       uint32_t live = 0;
       if (!done)
         live = fullm | tsb_decide_step(
@@ -656,7 +673,8 @@ k_raster_fwd(RasterParams p) {
                              L[4] = b.x; L[5] = b.y; L[6] = b.z; L[7] = b.w;
                              L[8] = c.x; L[9] = c.y; L[10] = c.z; L[11] = c.w;
                            },
-                           ws.sid, cand & ~fullm, zsm, lane, x, y, p.near_f, p.cam, p.m64, px, py);
+                           ws.sid, cand & ~fullm & ~zsm, 0u, lane, x, y, p.near_f, p.cam, p.m64,
+                           px, py, lc, uc);
 #ifdef TSB_STATS
       {
         const uint32_t nd = __ballot_sync(0xffffffffu, !done);

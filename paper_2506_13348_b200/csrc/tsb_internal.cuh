@@ -58,7 +58,8 @@ __device__ __forceinline__ uint32_t tsb_block_pixmask(uint32_t gbx, uint32_t gby
 // Live bits of one pixel (this lane) over the candidate mask `m` of a
 // staged step: the division-free pre-decision, two candidates per
 // iteration (independent chains), then the exact fp32 path and the fp64
-// guard band for the rare undecided pairs. `load_lin(k, L)` fills L[0..11]
+// guard band for the rare undecided pairs (live0 / und0: pairs already
+// pre-decided elsewhere, e.g. by tsb_decide_candidate). `load_lin(k, L)` fills L[0..11]
 // (tsb_make_lin's words) of staged entry k, `sid` holds the splat ids. The
 // result is exactly tsb_eval_lin + tsb_live_f64 of every candidate (tsb_math.h).
 // What the decide loop reads of staged entry k: the linear forms L0..L9
@@ -74,10 +75,13 @@ __device__ __forceinline__ uint32_t tsb_decide_step(DecAt dec_at, LoadLin load_l
                                                     const int32_t* sid, uint32_t m, uint32_t zs,
                                                     int lane, float x, float y, float near_f,
                                                     const tsb_cam_params& cam, const double* m64,
-                                                    int px, int py) {
+                                                    int px, int py, uint32_t live0 = 0,
+                                                    uint32_t und0 = 0) {
   uint32_t live = 0, undecided = 0;
   // z-safe candidates (kBlockZSafe): tsb_predecide_lin_nb reduces to the two
   // q tests (|D| > eps and the depth test hold on the whole block)
+  live = live0;
+  undecided = und0;
   for (uint32_t mz = m & zs; mz;) {
     int kk[TSB_DECIDE_ILP];
 #pragma unroll
@@ -128,6 +132,64 @@ __device__ __forceinline__ uint32_t tsb_decide_step(DecAt dec_at, LoadLin load_l
       r = tsb_live_f64(mm, mm[9], tsb_pixel_x(&cam, px), tsb_pixel_y(&cam, py), cam.near_z);
     }
     if (r) live |= 1u << k;
+  }
+  return live;
+}
+
+// 32x32 bit-matrix transpose across a warp: lane r holds row r (bit c =
+// element (r, c)); returns column `lane` (bit r = element (r, lane)). Five
+// butterfly stages of one shuffle each.
+__device__ __forceinline__ uint32_t tsb_warp_transpose32(uint32_t x, int lane) {
+  constexpr uint32_t kMask[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int s = 16 >> i;
+    const uint32_t m = kMask[i];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+  }
+  return x;
+}
+
+// Candidate-per-lane form of the z-safe part of tsb_decide_step: lane k
+// tests ITS staged splat (forms L0..L8 in g0..g2, r2hi = g2.w) at all 32
+// pixels of the 8x4 block with exactly the arithmetic of the per-pixel loop
+// (D = fmaf(L0, x, fmaf(L1, y, L2)), ...), so every q/D^2 test gives the same
+// bits; xs[c] are the block's fp32 column coordinates, row r's y comes from
+// lane 8r's `ylane` (every lane must call this). Returns the
+// pixels where the pair is surely live (bit row*8+col) and sets `und` to the
+// pixels in the annulus between the bounds (exact path). A warp instruction
+// here serves 32 candidates at once instead of one (no shared-memory loads).
+__device__ __forceinline__ uint32_t tsb_decide_candidate(const float4& g0, const float4& g1,
+                                                         const float4& g2, const float* xs,
+                                                         float ylane, uint32_t& und) {
+  const float r2hi = g2.w;
+  const float r2lo = tsb_lin_r2lo(r2hi);
+  uint32_t live = 0;
+  und = 0;
+#pragma unroll 1
+  for (int r = 0; r < 4; ++r) {
+    const float y = __shfl_sync(0xffffffffu, ylane, 8 * r);  // all lanes call this
+    const float Dr = fmaf(g0.y, y, g0.z);
+    const float Ur = fmaf(g1.x, y, g1.y);
+    const float Vr = fmaf(g1.w, y, g2.x);
+    uint32_t lrow = 0, urow = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float x = xs[c];
+      const float D = fmaf(g0.x, x, Dr);
+      const float Nu = fmaf(g0.w, x, Ur);
+      const float Nv = fmaf(g1.z, x, Vr);
+      const float q = fmaf(Nu, Nu, Nv * Nv);
+      const float D2 = D * D;
+      const bool sure = q <= r2lo * D2;
+      const bool maybe = q <= r2hi * D2;
+      const uint32_t bit = 1u << c;
+      if (sure) lrow |= bit;
+      if (maybe && !sure) urow |= bit;
+    }
+    live |= lrow << (8 * r);
+    und |= urow << (8 * r);
   }
   return live;
 }
