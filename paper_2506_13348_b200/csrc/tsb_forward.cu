@@ -1,28 +1,23 @@
 // tsb_forward.cu — forward render path for sm_100a.
 //
 //   K1 k_preprocess     per splat, fp64: rect/cull, centre depth key, M, frame,
-//                       SH radiance -> GeomRec / MatRec / fp64 M
-//   S1 depth sort       stable LSD radix sort of a 24-bit depth key (ids in
-//                       id order) + k_fix_runs: exact (fp64 z, id) order,
-//                       == np.lexsort((ids, z))
-//   K2 k_rank_counts    per rank: tile count, rank of id
-//   S2 exclusive scan   entry offsets in draw order
-//   K3 k_duplicate_lb   (tile, id) entries in draw order, binned by the test
-//                       box (rect ∩ alpha-cut ellipse box), load-balanced
-//   S3 tile sort        stable radix sort on tile bits only => per-tile lists
-//                       keep draw order (== keys (tile << 32) | rank)
-//   K4 k_ranges         [start, end) per tile
-//   K5 k_raster_fwd     CTA per tile: staged geometry in smem, fp32
-//                       intersection with fp64 guard band, TEX/verify/flat
-//                       texel fetch, 13-channel front-to-back composite
+//                       SH radiance -> GeomRec / MatRec / fp64 M; per-CTA
+//                       digit histograms of the depth key and of the entries'
+//                       tile columns / rows (difference arrays)
+//   S1 depth order      4 one-sweep passes + k_fix_runs (+ k_sort_long_runs):
+//                       exact (fp64 z, id) order == np.lexsort((ids, z))
+//   S2 tile lists       k_dup_tx (duplication fused with the tile-x pass) +
+//                       one-sweep tile-y pass => per-tile lists in draw order
+//   K4 k_ranges         [start, end) per tile          (S1, S2, K4: tsb_binning.cu)
+//   K5 k_raster_fwd     persistent warps over (tile, 8x4 block) units: staged
+//                       geometry in smem, fp32 intersection with fp64 guard
+//                       band, TEX/verify/flat texel fetch, 13-channel
+//                       front-to-back composite
 //   K6 k_shade          per pixel split-sum PBR (shading.py:126-183)
 //
 // Reference: /root/reference/pkg/src/texsplat/rasterize.py:127-438,
 // shading.py:51-183 (see tsb_math.h for line-level citations).
 
-#include <cub/block/block_scan.cuh>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -30,6 +25,7 @@
 #include <cstdio>
 #include <vector>
 
+#include "tsb_binning.cuh"
 #include "tsb_internal.cuh"
 
 // Rasterizer CTA shape: persistent warps, so any tile size runs with the
@@ -54,34 +50,25 @@ int cuda_fail(const char* what, cudaError_t err) {
 
 static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
-// Depth sort key width: 24 bits of (bits(z) - bits(near)) >> 32 (three
-// 8-bit radix passes); equal keys are re-ordered exactly by k_fix_runs.
-constexpr int kDepthKeyBits = 24;
-constexpr uint32_t kDepthCulled = (1u << kDepthKeyBits) - 1u;
-
 bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLayout* L) {
   if (P < 0 || W <= 0 || H <= 0 || cap < 0) return false;
   if (tile != 8 && tile != 16 && tile != 32) return false;
   L->tiles_x = (W + tile - 1) / tile;
   L->tiles_y = (H + tile - 1) / tile;
+  // entry keys (tile_y << 8 | tile_x): at most 256 tiles per axis
+  if (L->tiles_x > kMaxTileAxis || L->tiles_y > kMaxTileAxis) return false;
+  if (cap >= (int64_t)1 << 30) return false;  // look-back words hold 30-bit counts
   L->num_tiles = L->tiles_x * L->tiles_y;
   int bits = 1;
   while ((1ll << bits) <= (int64_t)L->num_tiles) ++bits;
   L->tile_bits = bits;
   const size_t Pn = (size_t)std::max(P, 1);
   const size_t C = (size_t)std::max<int64_t>(cap, 1);
-
-  // CUB temp storage (size queries only; nothing is launched).
-  size_t b_depth = 0, b_scan = 0, b_tile = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b_depth, (const uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (const int32_t*)nullptr,
-                                  (int32_t*)nullptr, (int)Pn, 0, kDepthKeyBits);
-  cub::DeviceScan::ExclusiveSum(nullptr, b_scan, (const int32_t*)nullptr,
-                                (int32_t*)nullptr, (int)Pn);
-  cub::DeviceRadixSort::SortPairs(nullptr, b_tile, (const uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (const int32_t*)nullptr,
-                                  (int32_t*)nullptr, (int)C, 0, bits);
-  L->cub_bytes = std::max(b_depth, std::max(b_scan, b_tile));
+  L->nb_depth = (int32_t)((Pn + kOsTileDepth - 1) / kOsTileDepth);
+  L->nb_dup = (int32_t)((Pn + kOsThreads - 1) / kOsThreads);
+  L->nb_tiley = (int32_t)((C + kOsTile - 1) / kOsTile);
+  L->status_words = kDepthPasses * pass_status_words(L->nb_depth) +
+                    pass_status_words(L->nb_dup) + pass_status_words(L->nb_tiley);
 
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
@@ -89,24 +76,25 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   L->rects = take(Pn * 8);
   L->mat = take(Pn * sizeof(MatRec));
   L->m64 = take(Pn * kM64Stride * sizeof(double));
-  L->dkeys_in = take(Pn * 8);
-  L->dkeys_out = take(Pn * 8);
+  L->dkeys_in = take(Pn * 8);   // full fp64 depth bits by id
+  L->dkeys_out = take(Pn * 8);  // scratch of k_sort_long_runs
   L->dk32_in = take(Pn * 4);
   L->dk32_out = take(Pn * 4);
   L->ids_in = take(Pn * 4);
-  L->ids_out = take(Pn * 4);
+  L->ids_out = take(Pn * 4);    // the draw order
   L->tile_count = take(Pn * 4);
-  L->counts_sorted = take(Pn * 4);
-  L->offsets = take(Pn * 4);
   L->rank = take(Pn * 4);
+  L->long_runs = take((Pn / (kShortRun + 2) + 1) * 8);
   L->ekeys_in = take(C * 4);
   L->ekeys_out = take(C * 4);
   L->evals_in = take(C * 4);
   L->evals_out = take(C * 4);
   L->ranges = take((size_t)L->num_tiles * 8);
   L->torder_out = take((size_t)L->num_tiles * 4);
+  // zeroed per frame as one block: counters, binning state, look-back words
   L->counters = take(64);
-  L->cub_tmp = take(L->cub_bytes);
+  L->bin = take(sizeof(BinCounters));
+  L->status = take(L->status_words * 4);
   L->total = o;
   return true;
 }
@@ -131,18 +119,31 @@ struct PrepParams {
   double* m64;
   uint64_t* dkeys;
   uint32_t* dkey32;
-  uint64_t near_bits;
+  uint32_t near_hi;      // high word of bits(near)
   int32_t* ids;
   int32_t* tile_count;
   const int32_t* slot;  // record storage permutation (tsb_scene.record_slot) or null
+  BinCounters* bin;     // digit histograms, kept count
+  int64_t* total;       // entries of the frame (counters[0])
 };
 
 #ifndef TSB_PREP_MINB
 #define TSB_PREP_MINB 3  // 80 registers: 3 CTAs/SM hide the fp64 and store latency
 #endif
 __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p) {
+  // per-CTA binning histograms (merged into p.bin with one atomic per non-zero bin)
+  __shared__ int32_t s_hd[kDepthPasses][kRadixBins];
+  __shared__ int32_t s_hx[kRadixBins + 1], s_hy[kRadixBins + 1];
+  __shared__ int32_t s_kept;
+  __shared__ unsigned long long s_total;
+  for (int i = threadIdx.x; i < kDepthPasses * (int)kRadixBins; i += blockDim.x)
+    (&s_hd[0][0])[i] = 0;
+  for (int i = threadIdx.x; i <= (int)kRadixBins; i += blockDim.x) s_hx[i] = s_hy[i] = 0;
+  if (threadIdx.x == 0) { s_kept = 0; s_total = 0ull; }
+  __syncthreads();
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= p.P) return;
+  uint32_t kkey = kDepthCulled32, kkept = 0, ktiles = 0;  // this splat's binning facts
+  if (id < p.P) {
   const int K = (p.sh_degree + 1) * (p.sh_degree + 1);
   double pos[3], tu[3], tv[3], s[2];
   for (int j = 0; j < 3; ++j) {
@@ -172,24 +173,34 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   // a strictly tighter, conservative version of _tile_lists' rect binning
   // (rasterize.py:246-258) — tiles outside it cannot hold a live pixel.
   const bool binned = r.keep && tb[1] > tb[0] && tb[3] > tb[2];
-  p.tile_count[id] = binned ? tsb_rect_tile_count(tb[0], tb[1], tb[2], tb[3], p.tile) : 0;
-  // 24-bit sort key: (bits(z) - bits(near)) >> 32 is monotone in z for
-  // z > near (positive doubles order like their bit patterns; 2^-20
-  // relative resolution over 16 binades, farther depths clamp); equal keys
-  // are re-ordered by k_fix_runs on the full 64-bit pattern, so the result
-  // is the exact (z, id) order.
+  int32_t ntiles = 0;
+  if (binned) {
+    const int tx0 = tb[0] / p.tile, tx1 = (tb[1] - 1) / p.tile;
+    const int ty0 = tb[2] / p.tile, ty1 = (tb[3] - 1) / p.tile;
+    const int nx = tx1 - tx0 + 1, ny = ty1 - ty0 + 1;
+    ntiles = nx * ny;
+    // entries per tile column / row as difference arrays (k_dup_tx, tile-y pass)
+    atomicAdd(&s_hx[tx0], ny);
+    atomicAdd(&s_hx[tx1 + 1], -ny);
+    atomicAdd(&s_hy[ty0], nx);
+    atomicAdd(&s_hy[ty1 + 1], -nx);
+  }
+  p.tile_count[id] = ntiles;
+  // 32-bit depth key: the high word of bits(z) minus that of bits(near) is
+  // monotone in z for z > near (positive doubles order like their bit
+  // patterns; 2^-20 relative resolution, no clamping); k_fix_runs re-orders
+  // equal keys by the full 64-bit pattern => the exact (z, id) order.
   const uint64_t full = tsb_f64_bits(r.view_z);
   p.dkeys[id] = r.keep ? full : ~0ull;
-  uint64_t k32 = kDepthCulled - 1;
-  if (r.keep) {
-    const uint64_t d = (full - p.near_bits) >> 32;
-    k32 = d < kDepthCulled - 1 ? d : kDepthCulled - 1;
-  }
-  p.dkey32[id] = r.keep ? (uint32_t)k32 : kDepthCulled;
+  const uint32_t k32 = r.keep ? (uint32_t)(full >> 32) - p.near_hi : kDepthCulled32;
+  p.dkey32[id] = k32;
   p.ids[id] = id;
+  kkey = k32;
+  kkept = r.keep ? 1 : 0;
+  ktiles = (uint32_t)ntiles;
   // the rasterizer and the backward read records only through tile-list
   // entries: splats without entries (culled, or no pixel in the box) skip them
-  if (!binned) return;
+  if (binned) {
   const int sl = p.slot ? p.slot[id] : id;  // records live at the splat's slot
   p.geom[sl] = g;
 
@@ -211,140 +222,36 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   double* m64 = p.m64 + (size_t)kM64Stride * id;  // the rare fp64 recheck: by id
   for (int k = 0; k < 9; ++k) m64[k] = r.m[k];
   m64[9] = op;
-}
-
-// S1b + K2: runs of equal 24-bit depth keys leave the stable sort in id
-// order; the thread at a run's start sorts the run by (full fp64 key, id) —
-// runs are rare and short for real scenes (insertion sort; already-sorted
-// runs cost one scan) — and then writes the tile count and rank of every
-// position of its run (singletons: their own). The culled tail (key
-// kDepthCulled) stays in id order.
-__global__ void k_fix_runs_rank(int32_t P, const uint32_t* __restrict__ k32,
-                                const uint64_t* __restrict__ k64, int32_t* __restrict__ ids,
-                                const int32_t* __restrict__ tile_count,
-                                int32_t* __restrict__ counts_sorted, int32_t* __restrict__ rank) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
-  const uint32_t k = k32[i];
-  const bool fixable = k != kDepthCulled;
-  if (fixable && i > 0 && k32[i - 1] == k) return;  // inside a run: its start handles it
-  int end = i;
-  if (fixable) {
-    while (end + 1 < P && k32[end + 1] == k) ++end;
-    for (int a = i + 1; a <= end; ++a) {
-      const int id = ids[a];
-      const uint64_t key = k64[id];
-      int b = a - 1;
-      while (b >= i) {
-        const int ob = ids[b];
-        const uint64_t kb = k64[ob];
-        if (kb < key || (kb == key && ob < id)) break;
-        ids[b + 1] = ob;
-        --b;
-      }
-      ids[b + 1] = id;
-    }
   }
-  for (int r = i; r <= end; ++r) {
-    const int id = ids[r];
-    counts_sorted[r] = tile_count[id];
-    rank[id] = r;
   }
-}
-
-// K3 (load-balanced): one thread per 4 consecutive output entries. The
-// owning draw-order rank of entry e is the last r with offsets[r] <= e
-// (binary search over the exclusive scan; zero-count ranks are skipped
-// because they share their successor's offset). Entries of a splat follow
-// its rect's tiles row by row, exactly like the per-splat loop above, and
-// each thread stores 4 keys + 4 ids as two 16-B vectors (coalesced).
-__global__ void __launch_bounds__(256) k_duplicate_lb(
-    int32_t P, int32_t tile, int32_t tiles_x, int64_t cap,
-    const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ counts_sorted,
-    const int32_t* __restrict__ offsets, const GeomRec* __restrict__ boxes,
-    const int32_t* __restrict__ slot, uint32_t* __restrict__ ekeys, int32_t* __restrict__ evals,
-    int64_t* __restrict__ counters) {
-  __shared__ int s_lo, s_hi;
-  const int64_t eb = 4 * (int64_t)blockIdx.x * blockDim.x;
-  const int64_t e0 = eb + 4 * threadIdx.x;
-  const int64_t total = (int64_t)offsets[P - 1] + counts_sorted[P - 1];
-  if (blockIdx.x == 0 && threadIdx.x == 0) counters[0] = total;
-  // owner ranks of the block's first and last entries: every thread's
-  // binary search then runs over ~100 ranks (L1 hits) instead of all P
-  if (total <= cap && eb < total) {
-    auto owner = [&](int64_t e) {
-      int lo = 0, hi = P;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(offsets + mid) <= e) lo = mid; else hi = mid;
-      }
-      return lo;
-    };
-    if (threadIdx.x == 0) s_lo = owner(eb);
-    if (threadIdx.x == 32) s_hi = owner(min(eb + 4 * (int64_t)blockDim.x, total) - 1) + 1;
-    __syncthreads();
-  }
-  if (e0 >= cap) return;
-  if (total > cap || e0 >= total) {  // padding: sorts after every real tile
-    if (e0 + 4 <= cap) {
-      *reinterpret_cast<uint4*>(ekeys + e0) = make_uint4(~0u, ~0u, ~0u, ~0u);
-    } else {
-      for (int64_t e = e0; e < cap; ++e) ekeys[e] = ~0u;
-    }
-    return;
-  }
-  // upper_bound(offsets, e0) - 1 within the block's owner range
-  int lo = s_lo, hi = s_hi;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(offsets + mid) <= e0) lo = mid; else hi = mid;
-  }
-  int r = lo, cur = -1;
-  uint32_t kq[4];
-  int32_t vq[4];
-  int id = 0, nxt = 1, ty0 = 0, tx0 = 0, off = 0;
+  // warp-aggregated histogram updates (equal digits of a warp: one atomic)
+  {
+    const int lane = threadIdx.x & 31;
+    const bool valid = id < p.P;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t e = e0 + q;
-    kq[q] = 0xFFFFFFFFu;
-    vq[q] = 0;
-    if (e >= total) continue;
-    // advance to the rank whose [offset, offset + count) holds e (zero-count
-    // ranks are skipped; terminates because e < total)
-    while (e >= (int64_t)__ldg(offsets + r) + __ldg(counts_sorted + r)) ++r;
-    if (r != cur) {
-      cur = r;
-      off = __ldg(offsets + r);
-      id = __ldg(sorted_ids + r);
-      if (slot) id = __ldg(slot + id);  // entries name the record slot
-      const uint32_t bx = __ldg(&boxes[id].bx), by = __ldg(&boxes[id].by);
-      const int x0 = bx & 0xFFFF, x1 = bx >> 16, y0 = by & 0xFFFF;
-      tx0 = x0 / tile;
-      nxt = (x1 - 1) / tile - tx0 + 1;
-      ty0 = y0 / tile;
+    for (int q = 0; q < kDepthPasses; ++q) {
+      const uint32_t d = valid ? (kkey >> (8 * q)) & 255u : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      if (valid && lane == __ffs(peers) - 1) atomicAdd(&s_hd[q][d], __popc(peers));
     }
-    const int j = (int)(e - off);
-    kq[q] = (uint32_t)((ty0 + j / nxt) * tiles_x + tx0 + j % nxt);
-    vq[q] = id;
+    const uint32_t nk = __reduce_add_sync(0xffffffffu, kkept);
+    const uint32_t nt = __reduce_add_sync(0xffffffffu, ktiles);
+    if (lane == 0 && nk) atomicAdd(&s_kept, (int)nk);
+    if (lane == 0 && nt) atomicAdd(&s_total, (unsigned long long)nt);
   }
-  if (e0 + 4 <= cap) {
-    *reinterpret_cast<uint4*>(ekeys + e0) = make_uint4(kq[0], kq[1], kq[2], kq[3]);
-    *reinterpret_cast<int4*>(evals + e0) = make_int4(vq[0], vq[1], vq[2], vq[3]);
-  } else {
-    for (int q = 0; q < 4 && e0 + q < cap; ++q) { ekeys[e0 + q] = kq[q]; evals[e0 + q] = vq[q]; }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kDepthPasses * (int)kRadixBins; i += blockDim.x) {
+    const int v = (&s_hd[0][0])[i];
+    if (v) atomicAdd(&(&p.bin->hist_depth[0][0])[i], v);
   }
-}
-
-// K4: tile ranges from the tile-sorted entry keys.
-__global__ void k_ranges(int64_t cap, const uint32_t* __restrict__ keys,
-                         const int64_t* __restrict__ counters, int32_t* __restrict__ ranges) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t total = counters[0];
-  if (total > cap) total = 0;  // overflowed frame: leave every tile empty
-  if (i >= total) return;
-  const uint32_t t = keys[i];
-  if (i == 0 || keys[i - 1] != t) ranges[2 * t] = (int32_t)i;
-  if (i == total - 1 || keys[i + 1] != t) ranges[2 * t + 1] = (int32_t)(i + 1);
+  for (int i = threadIdx.x; i <= (int)kRadixBins; i += blockDim.x) {
+    if (s_hx[i]) atomicAdd(&p.bin->hist_tx[i], s_hx[i]);
+    if (s_hy[i]) atomicAdd(&p.bin->hist_ty[i], s_hy[i]);
+  }
+  if (threadIdx.x == 0) {
+    if (s_kept) atomicAdd(&p.bin->kept, s_kept);
+    if (s_total) atomicAdd(reinterpret_cast<unsigned long long*>(p.total), s_total);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -753,9 +660,8 @@ constexpr int kSchedThreads = 1024;
 __global__ void __launch_bounds__(kSchedThreads) k_tile_schedule(int32_t nt,
                                                                  const int32_t* __restrict__ ranges,
                                                                  int32_t* __restrict__ order) {
-  using Scan = cub::BlockScan<int, kSchedThreads>;
-  __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int cursor[kSchedThreads];
+  __shared__ int wsum[kSchedThreads / 32];
   const int tid = threadIdx.x;
   cursor[tid] = 0;
   __syncthreads();
@@ -766,9 +672,26 @@ __global__ void __launch_bounds__(kSchedThreads) k_tile_schedule(int32_t nt,
   for (int t = tid; t < nt; t += kSchedThreads) atomicAdd(&cursor[bucket(t)], 1);
   __syncthreads();
   const int h = cursor[tid];
-  int start;
-  Scan(scan_tmp).ExclusiveSum(h, start);
-  cursor[tid] = start;
+  int x = h;  // block exclusive scan: warp scans, then a scan of the warp totals
+  const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    wsum[lane] = t;
+  }
+  __syncthreads();
+  cursor[tid] = (w ? wsum[w - 1] : 0) + x - h;
   __syncthreads();
   for (int t = tid; t < nt; t += kSchedThreads) order[atomicAdd(&cursor[bucket(t)], 1)] = t;
 }
@@ -968,26 +891,20 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
   cudaStream_t st = (cudaStream_t)stream;
   const tsb_cam_params cam = to_cam(camera);
   GeomRec* geom = ws_ptr<GeomRec>(ws, L.geom);
-  MatRec* mat = ws_ptr<MatRec>(ws, L.mat);
-  double* m64 = ws_ptr<double>(ws, L.m64);
-  uint64_t* dk_in = ws_ptr<uint64_t>(ws, L.dkeys_in);
-  uint64_t* dk_out = ws_ptr<uint64_t>(ws, L.dkeys_out);
-  int32_t* ids_in = ws_ptr<int32_t>(ws, L.ids_in);
-  int32_t* ids_out = ws_ptr<int32_t>(ws, L.ids_out);
+  uint64_t* dk64 = ws_ptr<uint64_t>(ws, L.dkeys_in);
+  uint32_t* k32a = ws_ptr<uint32_t>(ws, L.dk32_out);  // K1 writes here; the sorted keys end here
+  uint32_t* k32b = ws_ptr<uint32_t>(ws, L.dk32_in);
+  uint32_t* idsa = ws_ptr<uint32_t>(ws, L.ids_out);   // the draw order ends here
+  uint32_t* idsb = ws_ptr<uint32_t>(ws, L.ids_in);
   int32_t* tcount = ws_ptr<int32_t>(ws, L.tile_count);
-  int32_t* csorted = ws_ptr<int32_t>(ws, L.counts_sorted);
-  int32_t* offsets = ws_ptr<int32_t>(ws, L.offsets);
   int32_t* rank = ws_ptr<int32_t>(ws, L.rank);
-  uint32_t* ek_in = ws_ptr<uint32_t>(ws, L.ekeys_in);
-  uint32_t* ek_out = ws_ptr<uint32_t>(ws, L.ekeys_out);
-  int32_t* ev_in = ws_ptr<int32_t>(ws, L.evals_in);
-  int32_t* ev_out = ws_ptr<int32_t>(ws, L.evals_out);
   int32_t* ranges = ws_ptr<int32_t>(ws, L.ranges);
   int64_t* counters = ws_ptr<int64_t>(ws, L.counters);
-  void* cub_tmp = ws_ptr<char>(ws, L.cub_tmp);
-  size_t cub_bytes = L.cub_bytes;
+  BinCounters* bin = ws_ptr<BinCounters>(ws, L.bin);
+  uint32_t* status = ws_ptr<uint32_t>(ws, L.status);
 
-  TSB_CUDA(cudaMemsetAsync(counters, 0, 64, st));
+  // counters, binning state and look-back words are one contiguous block
+  TSB_CUDA(cudaMemsetAsync(counters, 0, L.status + L.status_words * 4 - L.counters, st));
   TSB_CUDA(cudaMemsetAsync(ranges, 0, (size_t)L.num_tiles * 8, st));
   if (P > 0) {
     PrepParams pp;
@@ -997,31 +914,75 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     pp.sc = scene->scales; pp.op = scene->opacities; pp.sh = scene->sh;
     pp.entries = mode == TSB_MODE_FLAT ? nullptr : atlas->entries;
     pp.T = atlas->resolution; pp.page_w = atlas->page_w; pp.page_h = atlas->page_h;
-    pp.geom = geom; pp.rects = ws_ptr<uint2>(ws, L.rects); pp.mat = mat; pp.m64 = m64; pp.dkeys = dk_in; pp.ids = ids_in;
-    pp.dkey32 = ws_ptr<uint32_t>(ws, L.dk32_in);
-    pp.near_bits = tsb_f64_bits(camera->near_z);
+    pp.geom = geom; pp.rects = ws_ptr<uint2>(ws, L.rects); pp.mat = ws_ptr<MatRec>(ws, L.mat);
+    pp.m64 = ws_ptr<double>(ws, L.m64); pp.dkeys = dk64;
+    pp.ids = reinterpret_cast<int32_t*>(idsa);
+    pp.dkey32 = k32a;
+    pp.near_hi = (uint32_t)(tsb_f64_bits(camera->near_z) >> 32);
     pp.tile_count = tcount;
     pp.slot = scene->record_slot;
+    pp.bin = bin;
+    pp.total = counters;
     k_preprocess<<<(P + 255) / 256, 256, 0, st>>>(pp);
     TSB_CHECK_LAUNCH("k_preprocess");
 
-    TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, ws_ptr<uint32_t>(ws, L.dk32_in),
-                                             ws_ptr<uint32_t>(ws, L.dk32_out), ids_in, ids_out,
-                                             P, 0, kDepthKeyBits, st));
-    k_fix_runs_rank<<<(P + 255) / 256, 256, 0, st>>>(P, ws_ptr<uint32_t>(ws, L.dk32_out), dk_in,
-                                                     ids_out, tcount, csorted, rank);
-    TSB_CHECK_LAUNCH("k_fix_runs_rank");
-    cub_bytes = L.cub_bytes;
-    TSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, csorted, offsets, P, st));
+    // S1: depth order (4 one-sweep passes a -> b -> a -> b -> a)
+    uint32_t* st_words = status;
+    for (int q = 0; q < kDepthPasses; ++q) {
+      OnesweepArgs oa;
+      const bool fwd = (q & 1) == 0;
+      oa.kin = fwd ? k32a : k32b; oa.vin = fwd ? idsa : idsb;
+      oa.kout = fwd ? k32b : k32a; oa.vout = fwd ? idsb : idsa;
+      oa.n = P; oa.n_dev = nullptr; oa.cap = 0;
+      oa.shift = 8 * q;
+      oa.hist = bin->hist_depth[q];
+      oa.hist_is_diff = 0;
+      oa.tiles_x = 0;
+      oa.status = st_words;
+      oa.nb = L.nb_depth;
+      oa.ticket = &bin->tickets[q];
+      k_onesweep<kOsItemsDepth><<<L.nb_depth, kOsThreads, 0, st>>>(oa);
+      TSB_CHECK_LAUNCH("k_onesweep(depth)");
+      st_words += pass_status_words(L.nb_depth);
+    }
+    FixRunsArgs fa;
+    fa.P = P; fa.k32 = k32a; fa.k64 = dk64; fa.ids = reinterpret_cast<int32_t*>(idsa);
+    fa.rank = rank; fa.n_long = &bin->n_long; fa.long_runs = ws_ptr<int32_t>(ws, L.long_runs);
+    k_fix_runs<<<(P + 255) / 256, 256, 0, st>>>(fa);
+    TSB_CHECK_LAUNCH("k_fix_runs");
+    LongRunArgs la;
+    la.n_long = &bin->n_long; la.long_runs = fa.long_runs; la.k64 = dk64;
+    la.ids = fa.ids; la.scratch = ws_ptr<int32_t>(ws, L.dkeys_out); la.rank = rank;
+    k_sort_long_runs<<<16, 128, 0, st>>>(la);
+    TSB_CHECK_LAUNCH("k_sort_long_runs");
+
+    // S2: tile lists (duplication fused with the tile-x pass, then tile-y)
+    DupArgs da;
+    da.sorted_ids = fa.ids; da.tile_count = tcount; da.slot = scene->record_slot; da.geom = geom;
+    da.kept = &bin->kept; da.total = counters; da.cap = cap; da.tile = tile;
+    da.hist_tx = bin->hist_tx;
+    da.kout = ws_ptr<uint32_t>(ws, L.ekeys_in); da.vout = ws_ptr<uint32_t>(ws, L.evals_in);
+    da.status = st_words;
+    da.nb = L.nb_dup;
+    da.ticket = &bin->tickets[4];
+    k_dup_tx<<<L.nb_dup, kOsThreads, 0, st>>>(da);
+    TSB_CHECK_LAUNCH("k_dup_tx");
+    st_words += pass_status_words(L.nb_dup);
+    OnesweepArgs ya;
+    ya.kin = da.kout; ya.vin = da.vout;
+    ya.kout = ws_ptr<uint32_t>(ws, L.ekeys_out); ya.vout = ws_ptr<uint32_t>(ws, L.evals_out);
+    ya.n = 0; ya.n_dev = counters; ya.cap = cap;
+    ya.shift = 8;
+    ya.hist = bin->hist_ty;
+    ya.hist_is_diff = 1;
+    ya.tiles_x = L.tiles_x;
+    ya.status = st_words;
+    ya.nb = L.nb_tiley;
+    ya.ticket = &bin->tickets[5];
+    k_onesweep<kOsItems><<<L.nb_tiley, kOsThreads, 0, st>>>(ya);
+    TSB_CHECK_LAUNCH("k_onesweep(tile_y)");
     const int64_t C = std::max<int64_t>(cap, 1);
-    k_duplicate_lb<<<(unsigned)((C + 1023) / 1024), 256, 0, st>>>(
-        P, tile, L.tiles_x, cap, ids_out, csorted, offsets, geom, scene->record_slot, ek_in, ev_in,
-        counters);
-    TSB_CHECK_LAUNCH("k_duplicate_lb");
-    cub_bytes = L.cub_bytes;
-    TSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, ek_in, ek_out, ev_in, ev_out,
-                                             (int)C, 0, L.tile_bits, st));
-    k_ranges<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(cap, ek_out, counters, ranges);
+    k_ranges<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(cap, ya.kout, counters, ranges);
     TSB_CHECK_LAUNCH("k_ranges");
   }
   if (entries_needed)
@@ -1418,7 +1379,7 @@ int tsb_frame_graph_launch(tsb_frame_graph_t g, const tsb_camera* camera, float*
   const tsb_cam_params cam = to_cam(camera);
   if (g->n_prep) {
     g->prep.cam = cam;
-    g->prep.near_bits = tsb_f64_bits(camera->near_z);
+    g->prep.near_hi = (uint32_t)(tsb_f64_bits(camera->near_z) >> 32);
     void* args[] = {&g->prep};
     cudaKernelNodeParams kp = g->kp_prep;
     kp.kernelParams = args;

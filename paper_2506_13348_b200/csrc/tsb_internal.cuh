@@ -323,9 +323,10 @@ struct AtlasTex {
 // Workspace carve-up; every offset is 256-B aligned.
 struct WsLayout {
   size_t geom, rects, mat, m64, dkeys_in, dkeys_out, dk32_in, dk32_out, ids_in, ids_out, tile_count,
-      counts_sorted, offsets, rank, ekeys_in, ekeys_out, evals_in, evals_out,
-      ranges, torder_out, counters, cub_tmp;
-  size_t cub_bytes;
+      rank, ekeys_in, ekeys_out, evals_in, evals_out, ranges, torder_out, counters, bin, status,
+      long_runs;
+  size_t status_words;                       // one-sweep look-back words (zeroed per frame)
+  int32_t nb_depth, nb_dup, nb_tiley;        // one-sweep CTAs per pass
   size_t total;
   int32_t tiles_x, tiles_y, num_tiles, tile_bits;
 };
