@@ -136,13 +136,14 @@ __device__ __forceinline__ void digit_offsets(const int32_t* hist, bool is_diff,
 }
 
 // Stable rank of this lane's item among the warp's items with the same digit
-// (digit kRadixBins = no item): running counter per (warp, digit), advanced
+// (digits 0..kRadixBins; kRadixBins + 1 = no item): running counter per
+// (warp, digit) — wrun has kRadixBins + 1 entries — advanced
 // by the group leader. Returns the counter value for this item.
 __device__ __forceinline__ uint32_t warp_rank(uint32_t* wrun, uint32_t d, int lane) {
   const uint32_t peers = __match_any_sync(0xffffffffu, d);
   const int leader = __ffs(peers) - 1;
   uint32_t old = 0;
-  if (lane == leader && d < kRadixBins) old = atomicAdd(&wrun[d], (uint32_t)__popc(peers));
+  if (lane == leader && d <= kRadixBins) old = atomicAdd(&wrun[d], (uint32_t)__popc(peers));
   old = __shfl_sync(0xffffffffu, old, leader);
   return old + (uint32_t)__popc(peers & ((1u << lane) - 1u));
 }
@@ -155,9 +156,11 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* wrun, uint32_t d, int la
 template <int ITEMS>
 __global__ void __launch_bounds__(kOsThreads) k_onesweep(OnesweepArgs a) {
   constexpr int TILE = kOsThreads * ITEMS;
-  __shared__ uint32_t whist[kOsWarps][kRadixBins];
+  constexpr uint32_t kCulledBin = kRadixBins;  // depth pass 1: culled items' own counter
+  __shared__ uint32_t whist[kOsWarps][kRadixBins + 1];
   __shared__ uint32_t s_goff[kRadixBins];
   __shared__ uint32_t s_warp[8];
+  __shared__ uint32_t s_culled_before;
   __shared__ int s_bid;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   int n = a.n;
@@ -165,9 +168,16 @@ __global__ void __launch_bounds__(kOsThreads) k_onesweep(OnesweepArgs a) {
     const int64_t e = *a.n_dev;
     n = e > a.cap ? 0 : (int)e;  // overflowed frame: nothing to sort
   }
+  // depth passes: items [0, K) are the kept splats (after pass 1), the culled
+  // tail [K, n) stays in id order; ranked items are those below `nr`
+  const int K = a.kept ? *a.kept : n;
+  const int nr = a.mode == kOsLater ? K : n;
   if (tid == 0) s_bid = atomicAdd(a.ticket, 1);
-  for (int i = tid; i < kOsWarps * kRadixBins; i += kOsThreads) (&whist[0][0])[i] = 0u;
+  for (int i = tid; i < kOsWarps * (int)(kRadixBins + 1); i += kOsThreads) (&whist[0][0])[i] = 0u;
   digit_offsets(a.hist, a.hist_is_diff, s_goff, s_warp);  // (syncs the block)
+  // a later depth pass whose digit is the same for every kept item is the identity
+  const bool trivial =
+      a.mode == kOsLater && __syncthreads_or(a.hist[tid] == K && K > 0);
   const int bid = s_bid;
   if (bid * TILE >= n) return;
   uint32_t key[ITEMS], val[ITEMS];
@@ -178,12 +188,26 @@ __global__ void __launch_bounds__(kOsThreads) k_onesweep(OnesweepArgs a) {
     key[r] = i < n ? a.kin[i] : 0u;
     val[r] = i < n ? a.vin[i] : 0u;
   }
-  // sweep 1: per-warp digit counts
+  if (trivial) {
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+      const int i = base + r * 32 + lane;
+      if (i < n) {
+        a.kout[i] = key[r];
+        a.vout[i] = val[r];
+      }
+    }
+    return;
+  }
+  // ranks within the warp (stable: rounds in order, lanes in order)
+  uint32_t rank[ITEMS];
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
-    const bool ok = base + r * 32 + lane < n;
-    const uint32_t d = ok ? (key[r] >> a.shift) & (kRadixBins - 1) : kRadixBins;
-    warp_rank(whist[w], d, lane);
+    const int i = base + r * 32 + lane;
+    uint32_t d = (key[r] >> a.shift) & (kRadixBins - 1);
+    if (a.mode == kOsFirst && key[r] == kDepthCulled32) d = kCulledBin;
+    if (i >= nr) d = kRadixBins + 1;  // no item / pass-through tail
+    rank[r] = warp_rank(whist[w], d, lane);
   }
   __syncthreads();
   {  // warp exclusive prefixes per digit, then the CTA's global offsets
@@ -197,20 +221,45 @@ __global__ void __launch_bounds__(kOsThreads) k_onesweep(OnesweepArgs a) {
     }
     const uint32_t excl = cta_prefix(a.status, a.nb, bid, d, c);
     s_goff[d] += excl;
+    if (a.mode == kOsFirst) {
+      // culled items before this CTA = items before it - kept items before it
+      uint32_t kb = excl;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) kb += __shfl_xor_sync(0xffffffffu, kb, o);
+      if (lane == 0) s_warp[w] = kb;
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t t = 0;
+        for (int v = 0; v < kOsWarps; ++v) t += s_warp[v];
+        s_culled_before = (uint32_t)(bid * TILE) - t;
+        uint32_t cw = 0;  // warp prefixes of the culled counter
+        for (int v = 0; v < kOsWarps; ++v) {
+          const uint32_t x = whist[v][kCulledBin];
+          whist[v][kCulledBin] = cw;
+          cw += x;
+        }
+      }
+    }
   }
   __syncthreads();
-  // sweep 2: stable scatter (running counters restart at the warp prefixes)
+  // stable scatter: CTA offset + warp prefix + rank within the warp
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
-    const bool ok = base + r * 32 + lane < n;
-    const uint32_t d = ok ? (key[r] >> a.shift) & (kRadixBins - 1) : kRadixBins;
-    const uint32_t pos = warp_rank(whist[w], d, lane) + (ok ? s_goff[d] : 0u);
-    if (ok) {
-      uint32_t k = key[r];
-      if (a.tiles_x > 0) k = (k >> 8) * (uint32_t)a.tiles_x + (k & 255u);  // -> tile index
-      a.kout[pos] = k;
-      a.vout[pos] = val[r];
+    const int i = base + r * 32 + lane;
+    if (i >= n) continue;
+    uint32_t pos;
+    if (i >= nr) {
+      pos = (uint32_t)i;  // the culled tail passes through
+    } else if (a.mode == kOsFirst && key[r] == kDepthCulled32) {
+      pos = (uint32_t)K + s_culled_before + whist[w][kCulledBin] + rank[r];
+    } else {
+      const uint32_t d = (key[r] >> a.shift) & (kRadixBins - 1);
+      pos = s_goff[d] + whist[w][d] + rank[r];
     }
+    uint32_t k = key[r];
+    if (a.tiles_x > 0) k = (k >> 8) * (uint32_t)a.tiles_x + (k & 255u);  // -> tile index
+    a.kout[pos] = k;
+    a.vout[pos] = val[r];
   }
 }
 
@@ -221,17 +270,19 @@ __global__ void __launch_bounds__(kOsThreads) k_onesweep(OnesweepArgs a) {
 // scatters (tile_y << 8 | tile_x, record slot) stably by tile_x.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kOsThreads) k_dup_tx(DupArgs a) {
-  __shared__ uint32_t whist[kOsWarps][kRadixBins];
+  __shared__ uint32_t whist[kOsWarps][kRadixBins + 1];
   __shared__ uint32_t s_goff[kRadixBins];
   __shared__ uint32_t s_base[kOsThreads + 33];
   __shared__ uint32_t s_box[kOsThreads];  // tx0 | ty0 << 8 | ntx << 16
   __shared__ int32_t s_slot[kOsThreads];
+  __shared__ uint32_t s_mag[kOsThreads];
+  __shared__ uint2 s_cache[kDupCache];
   __shared__ uint32_t s_warp[8];
   __shared__ int s_bid;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t E = *a.total;
   if (tid == 0) s_bid = atomicAdd(a.ticket, 1);
-  for (int i = tid; i < kOsWarps * kRadixBins; i += kOsThreads) (&whist[0][0])[i] = 0u;
+  for (int i = tid; i < kOsWarps * (int)(kRadixBins + 1); i += kOsThreads) (&whist[0][0])[i] = 0u;
   digit_offsets(a.hist_tx, true, s_goff, s_warp);
   const int bid = s_bid;
   const int K = *a.kept;
@@ -260,6 +311,8 @@ __global__ void __launch_bounds__(kOsThreads) k_dup_tx(DupArgs a) {
     s_base[ci] = base;
     s_box[ci] = box;
     s_slot[ci] = sl;
+    const uint32_t ntx = box >> 16;
+    s_mag[ci] = ntx > 1u ? (uint32_t)(0xFFFFFFFFull / ntx + 1ull) : 0u;
   }
   for (int i = (int)M + tid; i < kOsThreads + 33; i += kOsThreads) s_base[i] = 0xFFFFFFFFu;
   __syncthreads();
@@ -284,18 +337,21 @@ __global__ void __launch_bounds__(kOsThreads) k_dup_tx(DupArgs a) {
     o0 += __popc(pm) + (__any_sync(0xffffffffu, p == 32u) ? 1 : 0);
     const uint32_t bx = s_box[owner];
     const uint32_t ntx = bx >> 16, j = e0 + lane - s_base[owner];
-    uint32_t row = (uint32_t)((float)j * __frcp_rn((float)ntx));  // j / ntx, then exact
-    if (row * ntx > j) --row;
-    if ((row + 1) * ntx <= j) ++row;
+    // j / ntx: multiply-high by ceil(2^32 / ntx), exact for j, ntx < 2^16
+    const uint32_t row = ntx == 1u ? j : __umulhi(j, s_mag[owner]);
     key16 = (((bx >> 8) & 255u) + row) << 8 | ((bx & 255u) + (j - row * ntx));
     slot = s_slot[owner];
   };
+  // rank the entries; the CTA's entries (<= kDupCache) keep (key16 | rank << 16,
+  // slot) in shared memory for the scatter, larger CTAs recompute them
+  const bool cached = C <= (uint32_t)kDupCache;
   int o0 = o_lo;
-  for (uint32_t e0 = lo; e0 < hi; e0 += 32) {  // sweep 1: counts
+  for (uint32_t e0 = lo; e0 < hi; e0 += 32) {
     uint32_t k16;
     int32_t es;
     round(e0, o0, k16, es);
-    warp_rank(whist[w], e0 + lane < hi ? (k16 & 255u) : kRadixBins, lane);
+    const uint32_t rk = warp_rank(whist[w], e0 + lane < hi ? (k16 & 255u) : kRadixBins + 1, lane);
+    if (cached && e0 + lane < hi) s_cache[e0 + lane] = make_uint2(k16 | (rk << 16), (uint32_t)es);
   }
   __syncthreads();
   {
@@ -310,13 +366,25 @@ __global__ void __launch_bounds__(kOsThreads) k_dup_tx(DupArgs a) {
     s_goff[d] += cta_prefix(a.status, a.nb, bid, d, c);
   }
   __syncthreads();
+  if (cached) {
+    for (uint32_t e = tid; e < C; e += kOsThreads) {
+      const uint2 c = s_cache[e];
+      const uint32_t k16 = c.x & 0xFFFFu, d = k16 & 255u;
+      // the warp that ranked entry e: the last w with floor(C w / 8) <= e
+      const int we = (int)(((uint64_t)(e + 1) * kOsWarps - 1) / C);
+      const uint32_t pos = s_goff[d] + whist[we][d] + (c.x >> 16);
+      a.kout[pos] = k16;
+      a.vout[pos] = c.y;
+    }
+    return;
+  }
   o0 = o_lo;
-  for (uint32_t e0 = lo; e0 < hi; e0 += 32) {  // sweep 2: stable scatter
+  for (uint32_t e0 = lo; e0 < hi; e0 += 32) {  // (uncached) sweep 2: stable scatter
     const uint32_t e = e0 + lane;
     uint32_t k16;
     int32_t es;
     round(e0, o0, k16, es);
-    const uint32_t d = e < hi ? (k16 & 255u) : kRadixBins;
+    const uint32_t d = e < hi ? (k16 & 255u) : kRadixBins + 1;
     const uint32_t pos = warp_rank(whist[w], d, lane) + (e < hi ? s_goff[d] : 0u);
     if (e < hi) {
       a.kout[pos] = k16;
@@ -372,7 +440,7 @@ __global__ void k_fix_runs(FixRunsArgs a) {
 // key (the high word is the run's common key), ids ping-ponging through
 // `scratch`. O(run) per pass; then the ranks.
 __global__ void __launch_bounds__(128) k_sort_long_runs(LongRunArgs a) {
-  __shared__ uint32_t run_ctr[4][kRadixBins];
+  __shared__ uint32_t run_ctr[4][kRadixBins + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * 4 + w, nw = gridDim.x * 4;
   const int nl = *a.n_long;
@@ -393,7 +461,7 @@ __global__ void __launch_bounds__(128) k_sort_long_runs(LongRunArgs a) {
         __syncwarp();
         for (int q0 = 0; q0 < len; q0 += 32) {  // histogram
           const int q = q0 + lane;
-          const uint32_t d = q < len ? ((uint32_t)a.k64[src[q]] >> (8 * pass)) & 255u : kRadixBins;
+          const uint32_t d = q < len ? ((uint32_t)a.k64[src[q]] >> (8 * pass)) & 255u : kRadixBins + 1;
           warp_rank(ctr, d, lane);
         }
         __syncwarp();
@@ -421,7 +489,7 @@ __global__ void __launch_bounds__(128) k_sort_long_runs(LongRunArgs a) {
         for (int q0 = 0; q0 < len; q0 += 32) {  // stable scatter
           const int q = q0 + lane;
           const int id = q < len ? src[q] : 0;
-          const uint32_t d = q < len ? ((uint32_t)a.k64[id] >> (8 * pass)) & 255u : kRadixBins;
+          const uint32_t d = q < len ? ((uint32_t)a.k64[id] >> (8 * pass)) & 255u : kRadixBins + 1;
           const uint32_t pos = warp_rank(ctr, d, lane);
           if (q < len) dst[pos] = id;
         }
@@ -435,8 +503,8 @@ __global__ void __launch_bounds__(128) k_sort_long_runs(LongRunArgs a) {
   }
 }
 
-template __global__ void k_onesweep<kOsItemsDepth>(OnesweepArgs a);
-template __global__ void k_onesweep<kOsItems>(OnesweepArgs a);
+template __global__ void k_onesweep<8>(OnesweepArgs a);
+template __global__ void k_onesweep<16>(OnesweepArgs a);
 
 // K4: tile ranges from the tile-sorted entry keys.
 __global__ void k_ranges(int64_t cap, const uint32_t* __restrict__ keys,

@@ -12,10 +12,11 @@ constexpr int kRadixBits = 8;
 constexpr uint32_t kRadixBins = 1u << kRadixBits;
 constexpr int kOsThreads = 256;   // one-sweep CTA: 8 warps, one digit per thread
 constexpr int kOsWarps = kOsThreads / 32;
-constexpr int kOsItems = 16;      // items per thread (tile-y pass)
+constexpr int kOsItems = 8;       // items per thread (tile-y pass)
 constexpr int kOsTile = kOsThreads * kOsItems;
 constexpr int kOsItemsDepth = 8;  // depth passes: P is small, more CTAs in flight
 constexpr int kOsTileDepth = kOsThreads * kOsItemsDepth;
+constexpr int kDupCache = 3072;  // entries of a k_dup_tx CTA kept in shared memory
 constexpr int kDepthPasses = 4;   // 32-bit depth key, 8-bit digits
 constexpr uint32_t kDepthCulled32 = 0xFFFFFFFFu;
 constexpr int kShortRun = 32;     // runs of equal 32-bit keys up to 33 long: one thread
@@ -32,6 +33,10 @@ struct BinCounters {
   int32_t hist_ty[kRadixBins + 1];               // tile columns / rows
 };
 
+constexpr int32_t kOsPlain = 0;  // (tile-y pass)
+constexpr int32_t kOsFirst = 1;  // depth pass 1: culled items (key 0xFFFFFFFF) to the tail
+constexpr int32_t kOsLater = 2;  // depth passes 2-4: rank [0, K), the tail passes through
+
 struct OnesweepArgs {
   const uint32_t* kin;
   const uint32_t* vin;
@@ -46,6 +51,8 @@ struct OnesweepArgs {
   int32_t tiles_x;       // > 0: output key (ty << 8 | tx) -> tile index ty * tiles_x + tx
   uint32_t* status;      // pass_status_words(nb) words
   int32_t nb;            // CTAs of the pass (grid size)
+  int32_t mode;          // kOsPlain / kOsFirst / kOsLater
+  const int32_t* kept;   // depth passes: the kept count K (device)
   int32_t* ticket;
 };
 

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   const uint32_t k32 = r.keep ? (uint32_t)(full >> 32) - p.near_hi : kDepthCulled32;
   p.dkey32[id] = k32;
   p.ids[id] = id;
-  kkey = k32;
+  kkey = k32;  // (the depth histograms count kept splats only)
   kkept = r.keep ? 1 : 0;
   ktiles = (uint32_t)ntiles;
   // the rasterizer and the backward read records only through tile-list
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   // warp-aggregated histogram updates (equal digits of a warp: one atomic)
   {
     const int lane = threadIdx.x & 31;
-    const bool valid = id < p.P;
+    const bool valid = id < p.P && kkept;
 #pragma unroll
     for (int q = 0; q < kDepthPasses; ++q) {
       const uint32_t d = valid ? (kkey >> (8 * q)) & 255u : 256u;
@@ -940,6 +940,8 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
       oa.tiles_x = 0;
       oa.status = st_words;
       oa.nb = L.nb_depth;
+      oa.mode = q == 0 ? kOsFirst : kOsLater;
+      oa.kept = &bin->kept;
       oa.ticket = &bin->tickets[q];
       k_onesweep<kOsItemsDepth><<<L.nb_depth, kOsThreads, 0, st>>>(oa);
       TSB_CHECK_LAUNCH("k_onesweep(depth)");
@@ -978,6 +980,8 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     ya.tiles_x = L.tiles_x;
     ya.status = st_words;
     ya.nb = L.nb_tiley;
+    ya.mode = kOsPlain;
+    ya.kept = nullptr;
     ya.ticket = &bin->tickets[5];
     k_onesweep<kOsItems><<<L.nb_tiley, kOsThreads, 0, st>>>(ya);
     TSB_CHECK_LAUNCH("k_onesweep(tile_y)");
