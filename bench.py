@@ -286,12 +286,15 @@ def main():
                  texel_format=args.texel_format, tile=args.tile)
     my_views = [cams[i] for i in range(rank, len(cams), world)]
 
-    # size the workspace from the whole orbit once (no per-frame host sync)
+    # size the workspace from every view of this rank once (no per-frame host
+    # sync later); the device-side running maximum of the entry counts
+    # (k_ranges) then guards every timed / phased / e2e frame
     need = 0
-    for cam in my_views[:: max(1, len(my_views) // 16)]:
+    for cam in my_views:
         r.render(cam, check=True)
         need = max(need, r.entries_needed())
-    r.reserve(my_views[0], int(need * 1.15) + 4096)
+    r.reserve(my_views[0], int(need * 1.25) + 4096)
+    r.prep.workspace.reset_max()
 
     W, H = args.width, args.height
     gb, px, col, _, _ = r._buffers(W, H)
@@ -372,7 +375,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    overflow = r.entries_needed() > ws.capacity
+    overflow = r.max_entries_needed() > ws.capacity  # any phased or timed frame
     fragments = int(frag_total.item()) / KB
 
     # ---- e2e: public API, host result every step ---------------------------

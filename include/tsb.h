@@ -115,6 +115,15 @@ typedef struct tsb_pixel_state {
 int tsb_frame_workspace_size(int32_t num_splats, int32_t width, int32_t height,
                              int32_t tile, int64_t max_entries, uint64_t* bytes);
 
+/* Byte offset, inside the same workspace, of the int64 running maximum of
+ * the entries needed by every frame binned into it since the caller last
+ * zeroed it (the per-frame counters are reset by each frame; this word is
+ * not). A frame graph replayed without a host check can compare it with
+ * max_entries afterwards: larger means some frame overflowed (rendered with
+ * empty tile lists) and must be re-rendered with a larger workspace. */
+int tsb_frame_workspace_max_needed_offset(int32_t num_splats, int32_t width, int32_t height,
+                                          int32_t tile, int64_t max_entries, uint64_t* offset);
+
 /* Whole forward pass K1-K5 (replaces rasterize.prepare rasterize.py:172-243,
  * _tile_lists :246-258 and render_forward :395-438): preprocess, fp64
  * depth-rank sort, tile duplication, stable tile sort, tile ranges and the

@@ -91,6 +91,8 @@ _P = C.c_void_p
 _SIGNATURES = {
     "tsb_frame_workspace_size": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64,
                                  C.POINTER(C.c_uint64)],
+    "tsb_frame_workspace_max_needed_offset": [C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_int64, C.POINTER(C.c_uint64)],
     "tsb_render_forward": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
                            C.c_int32, C.c_int32, _P, C.c_uint64, C.c_int64, _P,
                            C.POINTER(PixelState_t), _P, _P],

@@ -97,6 +97,7 @@ def splat_backward(scene, camera, prep, tape: Tape, dbuf, *, grads: SceneGrads =
     del scene
     if tape.mode != _lib.MODE_VERIFY or tape.prep.texture_mode == "flat":
         raise ValueError("gradients require the per-primitive texture path")
+    tape.check_current()
     prep = prep if prep is not None else tape.prep
     dev = tape.gbuf.device
     H, W = int(camera.height), int(camera.width)

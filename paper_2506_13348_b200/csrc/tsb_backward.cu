@@ -963,16 +963,19 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera, const 
   rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);
   TSB_CUDA(cudaMemsetAsync(rp.work_counter, 0, 4, st));
   const size_t smem = 8 * sizeof(BwdWarpSmem);
-  static int resident = 0;
-  if (!resident) {
-    int dev = 0, sms = 0, per_sm = 0;
-    TSB_CUDA(cudaFuncSetAttribute(k_raster_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    TSB_CUDA(cudaGetDevice(&dev));
-    TSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_bwd, 256, smem));
-    resident = sms * (per_sm > 0 ? per_sm : 1);
-  }
+  static PerDevice s_resident;  // per device: attributes set, persistent grid size
+  int resident = 0;
+  TSB_CUDA(s_resident.get(
+      [smem](int dev) {
+        int sms = 0, per_sm = 0;
+        cudaError_t e = cudaFuncSetAttribute(k_raster_bwd,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess)
+          e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_bwd, 256, smem);
+        return e == cudaSuccess ? sms * (per_sm > 0 ? per_sm : 1) : -(int)e;
+      },
+      &resident));
   const int units = L.num_tiles * (tile * tile / 32);
   k_raster_bwd<<<std::min((units + 7) / 8, resident), 256, smem, st>>>(rp);
   TSB_CHECK_LAUNCH("k_raster_bwd");

@@ -508,9 +508,12 @@ template __global__ void k_onesweep<16>(OnesweepArgs a);
 
 // K4: tile ranges from the tile-sorted entry keys.
 __global__ void k_ranges(int64_t cap, const uint32_t* __restrict__ keys,
-                         const int64_t* __restrict__ counters, int32_t* __restrict__ ranges) {
+                         const int64_t* __restrict__ counters, int32_t* __restrict__ ranges,
+                         int64_t* __restrict__ max_needed) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = counters[0];
+  if (i == 0)  // running max over frames (tsb_frame_workspace_max_needed_offset)
+    atomicMax(reinterpret_cast<unsigned long long*>(max_needed), (unsigned long long)total);
   if (total > cap) total = 0;  // overflowed frame: leave every tile empty
   if (i >= total) return;
   const uint32_t t = keys[i];

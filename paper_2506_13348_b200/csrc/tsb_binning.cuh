@@ -104,6 +104,7 @@ __global__ void k_dup_tx(DupArgs a);
 __global__ void k_fix_runs(FixRunsArgs a);
 __global__ void k_sort_long_runs(LongRunArgs a);
 __global__ void k_ranges(int64_t cap, const uint32_t* __restrict__ keys,
-                         const int64_t* __restrict__ counters, int32_t* __restrict__ ranges);
+                         const int64_t* __restrict__ counters, int32_t* __restrict__ ranges,
+                         int64_t* __restrict__ max_needed);
 
 }  // namespace tsb

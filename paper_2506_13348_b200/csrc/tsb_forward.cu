@@ -91,6 +91,7 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   L->evals_out = take(C * 4);
   L->ranges = take((size_t)L->num_tiles * 8);
   L->torder_out = take((size_t)L->num_tiles * 4);
+  L->max_needed = take(8);  // running max over frames (never reset by a frame)
   // zeroed per frame as one block: counters, binning state, look-back words
   L->counters = take(64);
   L->bin = take(sizeof(BinCounters));
@@ -781,26 +782,27 @@ template <int TILE, int MODE>
 inline cudaError_t launch_raster_mode(int blocks, cudaStream_t st, const RasterParams& rp) {
   constexpr int threads = 32 * TSB_RASTER_WARPS;
   const size_t smem = (size_t)(threads / 32) * kRasterWarpSmem<MODE>;
-  static int resident = 0;  // per instantiation: persistent grid size
-  if (!resident) {
-    cudaError_t e = cudaFuncSetAttribute(k_raster_fwd<TILE, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    // the smallest shared-memory carveout that holds the resident CTAs: the
-    // rest of the 256 KB stays L1, which caches the atlas texels
-    e = cudaFuncSetAttribute(k_raster_fwd<TILE, MODE>,
-                             cudaFuncAttributePreferredSharedMemoryCarveout,
-                             MODE == TSB_MODE_VERIFY ? -1 : TSB_RASTER_CARVEOUT);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
-      return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_fwd<TILE, MODE>,
-                                                           threads, smem)) != cudaSuccess)
-      return e;
-    resident = std::max(1, sms * per_sm);
-  }
+  static PerDevice s_resident;  // per instantiation and device: persistent grid size
+  int resident = 0;
+  cudaError_t e = s_resident.get(
+      [smem](int dev) {
+        cudaError_t r = cudaFuncSetAttribute(k_raster_fwd<TILE, MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // the smallest shared-memory carveout that holds the resident CTAs: the
+        // rest of the 256 KB stays L1, which caches the atlas texels
+        if (r == cudaSuccess)
+          r = cudaFuncSetAttribute(k_raster_fwd<TILE, MODE>,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   MODE == TSB_MODE_VERIFY ? -1 : TSB_RASTER_CARVEOUT);
+        int sms = 0, per_sm = 0;
+        if (r == cudaSuccess) r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (r == cudaSuccess)
+          r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_fwd<TILE, MODE>,
+                                                            threads, smem);
+        return r == cudaSuccess ? std::max(1, sms * per_sm) : -(int)r;
+      },
+      &resident);
+  if (e != cudaSuccess) return e;
   // one warp per (tile, 8x4 block) unit at most
   const int units = blocks * (TILE * TILE / 32);
   const int grid = std::min((units + TSB_RASTER_WARPS - 1) / TSB_RASTER_WARPS, resident);
@@ -832,10 +834,22 @@ int tsb_frame_workspace_size(int32_t P, int32_t W, int32_t H, int32_t tile, int6
                              uint64_t* bytes) {
   WsLayout L;
   if (!bytes || !ws_layout(P, W, H, tile, cap, &L)) {
-    set_error("tsb_frame_workspace_size: invalid arguments");
+    set_error("tsb_frame_workspace_size: invalid arguments (tile 8/16/32, at most 256 tiles "
+              "per image axis, max_entries < 2^30)");
     return TSB_ERR_VALUE;
   }
   *bytes = L.total;
+  return TSB_OK;
+}
+
+int tsb_frame_workspace_max_needed_offset(int32_t P, int32_t W, int32_t H, int32_t tile,
+                                          int64_t cap, uint64_t* offset) {
+  WsLayout L;
+  if (!offset || !ws_layout(P, W, H, tile, cap, &L)) {
+    set_error("tsb_frame_workspace_max_needed_offset: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  *offset = L.max_needed;
   return TSB_OK;
 }
 
@@ -986,7 +1000,8 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     k_onesweep<kOsItems><<<L.nb_tiley, kOsThreads, 0, st>>>(ya);
     TSB_CHECK_LAUNCH("k_onesweep(tile_y)");
     const int64_t C = std::max<int64_t>(cap, 1);
-    k_ranges<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(cap, ya.kout, counters, ranges);
+    k_ranges<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(cap, ya.kout, counters, ranges,
+                                                          ws_ptr<int64_t>(ws, L.max_needed));
     TSB_CHECK_LAUNCH("k_ranges");
   }
   if (entries_needed)

@@ -6,6 +6,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/tsb.h"
@@ -323,8 +324,8 @@ struct AtlasTex {
 // Workspace carve-up; every offset is 256-B aligned.
 struct WsLayout {
   size_t geom, rects, mat, m64, dkeys_in, dkeys_out, dk32_in, dk32_out, ids_in, ids_out, tile_count,
-      rank, ekeys_in, ekeys_out, evals_in, evals_out, ranges, torder_out, counters, bin, status,
-      long_runs;
+      rank, ekeys_in, ekeys_out, evals_in, evals_out, ranges, torder_out, max_needed, counters,
+      bin, status, long_runs;
   size_t status_words;                       // one-sweep look-back words (zeroed per frame)
   int32_t nb_depth, nb_dup, nb_tiley;        // one-sweep CTAs per pass
   size_t total;
@@ -332,6 +333,31 @@ struct WsLayout {
 };
 
 bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLayout* L);
+
+// One-time per-device setup (function attributes, __constant__ uploads,
+// persistent grid sizes): one value per device ordinal, computed on first
+// use on that device, thread-safe. `init` returns > 0 on success, or a
+// negative cudaError_t.
+constexpr int kMaxDevices = 64;
+struct PerDevice {
+  std::mutex m;
+  int val[kMaxDevices] = {};
+  template <class F>
+  cudaError_t get(F&& init, int* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lock(m);
+    if (val[dev] <= 0) {
+      const int v = init(dev);
+      if (v <= 0) return v < 0 ? (cudaError_t)(-v) : cudaErrorUnknown;
+      val[dev] = v;
+    }
+    *out = val[dev];
+    return cudaSuccess;
+  }
+};
 
 void set_error(const std::string& msg);
 int cuda_fail(const char* what, cudaError_t err);

@@ -589,21 +589,26 @@ __global__ void k_orthonormalize(int32_t P, double* __restrict__ tu, double* __r
   for (int k = 0; k < 3; ++k) { tu[3 * i + k] = u[k]; tv[3 * i + k] = v[k] / nv; }
 }
 
-bool g_win_ready = false;
+// The SSIM window lives in per-device __constant__ memory: uploaded once per
+// device (a second GPU in the same process gets its own copy).
+PerDevice g_win;
 
 cudaError_t ensure_window() {
-  if (g_win_ready) return cudaSuccess;
-  float w[2 * kR + 1];
-  double s = 0.0, wd[2 * kR + 1];
-  for (int i = 0; i <= 2 * kR; ++i) {
-    const double x = (double)(i - kR);
-    wd[i] = std::exp(-0.5 * (x / 1.5) * (x / 1.5));
-    s += wd[i];
-  }
-  for (int i = 0; i <= 2 * kR; ++i) w[i] = (float)(wd[i] / s);
-  cudaError_t e = cudaMemcpyToSymbol(c_win, w, sizeof(w));
-  if (e == cudaSuccess) g_win_ready = true;
-  return e;
+  int ok = 0;
+  return g_win.get(
+      [](int) {
+        float w[2 * kR + 1];
+        double s = 0.0, wd[2 * kR + 1];
+        for (int i = 0; i <= 2 * kR; ++i) {
+          const double x = (double)(i - kR);
+          wd[i] = std::exp(-0.5 * (x / 1.5) * (x / 1.5));
+          s += wd[i];
+        }
+        for (int i = 0; i <= 2 * kR; ++i) w[i] = (float)(wd[i] / s);
+        const cudaError_t e = cudaMemcpyToSymbol(c_win, w, sizeof(w));
+        return e == cudaSuccess ? 1 : -(int)e;
+      },
+      &ok);
 }
 
 }  // namespace

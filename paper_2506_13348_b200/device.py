@@ -268,7 +268,13 @@ class DeviceEnvironment:
 
 class FrameWorkspace:
     """Frame workspace (sort buffers, per-splat records, tile lists) sized for
-    `capacity` splat x tile entries; grown when a frame needs more."""
+    `capacity` splat x tile entries; grown when a frame needs more.
+
+    `needed` (device int64) receives each frame's entry count; `max_needed`
+    is the device-side running maximum over every frame binned since the
+    last `reset_max()` (tsb_frame_workspace_max_needed_offset), so frames
+    replayed without a host check can be validated afterwards. `generation`
+    counts the frames rendered into the workspace (a Tape remembers its own)."""
 
     def __init__(self, device=None):
         self.device = _dev(device)
@@ -277,23 +283,42 @@ class FrameWorkspace:
         self.buf = None
         self.nbytes = 0
         self.needed = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.max_needed = None
+        self.generation = 0
         self.shrink_to = None
 
     def ensure(self, P, W, H, tile, capacity, exact: bool = False):
-        """Make room for `capacity` entries. The binning sorts the whole
-        capacity (padding included), so `exact=True` also shrinks."""
+        """Make room for `capacity` entries (`exact=True` also shrinks)."""
         key = (P, W, H, tile)
         if self.key == key and (self.capacity == capacity or
                                 (not exact and self.capacity >= capacity)):
             return
         cap = max(int(capacity), 1)
-        nb = C.c_uint64()
-        _lib.check(_lib.lib().tsb_frame_workspace_size(P, W, H, tile, cap, C.byref(nb)),
+        nb, off = C.c_uint64(), C.c_uint64()
+        L = _lib.lib()
+        _lib.check(L.tsb_frame_workspace_size(P, W, H, tile, cap, C.byref(nb)),
                    "tsb_frame_workspace_size")
+        _lib.check(L.tsb_frame_workspace_max_needed_offset(P, W, H, tile, cap, C.byref(off)),
+                   "tsb_frame_workspace_max_needed_offset")
         self.buf = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
         self.nbytes = int(nb.value)
+        o = int(off.value)
+        self.max_needed = self.buf[o:o + 8].view(torch.int64)
+        self.max_needed.zero_()
         self.capacity = cap
         self.key = key
+        self.generation += 1
+
+    def reset_max(self):
+        if self.max_needed is not None:
+            self.max_needed.zero_()
+
+    def max_needed_value(self) -> int:
+        """Largest entry count of any frame since reset_max() (host sync)."""
+        return 0 if self.max_needed is None else int(self.max_needed.item())
+
+    def overflowed(self) -> bool:
+        return self.max_needed_value() > self.capacity
 
     @staticmethod
     def initial_capacity(P, W, H, tile):

@@ -3,8 +3,10 @@
 Reference: environment.py:28-464. The per-frame samplers run on the GPU
 inside k_shade (tsb_math.h tsb_sample_equirect / tsb_sample_specular /
 tsb_sample_lut). This module holds the host-side containers and the one-time
-precompute (GGX prefilter, cosine irradiance, split-sum LUT), restated in
-vectorised numpy; SURVEY.md §8(f) ranks moving these to the GPU later.
+precompute (GGX prefilter, cosine irradiance, split-sum LUT). The precompute
+runs on the GPU (K15 tsb_env_prefilter, K16 tsb_brdf_lut; pass `device=`);
+the vectorised numpy restatement kept here is the host checker those kernels
+are tested against (bit-identical to the reference's numpy).
 """
 
 from __future__ import annotations
@@ -203,7 +205,7 @@ class BrdfLut:
     @staticmethod
     def build(resolution: int = 64, samples: int = 2048, device=None) -> "BrdfLut":
         """BrdfLut.build (environment.py:381-390). With `device` the table is
-        integrated on the GPU (K17, tsb_brdf_lut)."""
+        integrated on the GPU (K16, tsb_brdf_lut)."""
         if device is not None:
             import torch
 

@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, resident
 from .device import DeviceAtlas, DeviceScene, FrameWorkspace
 from .scene import scene_texels
 
@@ -148,6 +148,16 @@ class Tape:
     gbuf: torch.Tensor
     mode: int = 0
     extra: dict = field(default_factory=dict)
+    generation: int = 0  # the workspace's frame counter when this tape was taken
+
+    def check_current(self):
+        """The tape's tile lists and records live in the shared frame
+        workspace; a later frame rendered into it invalidates them."""
+        ws = self.prep.workspace
+        if ws is None or ws.generation != self.generation or ws.buf is not self.workspace:
+            raise RuntimeError("stale tape: another frame was rendered into this prepared "
+                               "scene's workspace after it (render again with_tape=True, or "
+                               "use a separate prepare() per pending backward)")
 
 
 def _resolve_sampler(texture_mode, sampler):
@@ -170,13 +180,23 @@ def prepare(scene, camera=None, texture_mode: str = "perprim", atlas_set=None, *
     if texture_mode not in ("flat", "perprim", "atlas"):
         raise ValueError(f"unknown texture mode {texture_mode!r}")
     smp = _resolve_sampler(texture_mode, sampler)
-    dscene = scene if isinstance(scene, DeviceScene) else DeviceScene(scene, device)
+    dkey = (str(device),)
+    # device copies are cached per host object (resident.py): repeated calls
+    # with the same scene / atlas objects upload nothing
+    if isinstance(scene, DeviceScene):
+        dscene = scene
+    else:
+        geo = resident.scene_arrays(scene)[:6]
+        dscene = resident.cached("scene", scene, dkey, geo, lambda: DeviceScene(scene, device))
     T = dscene.texture_resolution
     if texture_mode == "flat":
-        datlas = DeviceAtlas.flat_only(scene_texels(scene), device)
+        datlas = resident.cached("flat", scene, dkey, resident.scene_arrays(scene)[6:],
+                                 lambda: DeviceAtlas.flat_only(scene_texels(scene), device))
     elif texture_mode == "perprim":
-        datlas = DeviceAtlas(texels=scene_texels(scene), linear=(smp == "verify"),
-                             hw=(smp == "hw"), texel_format=texel_format, device=device)
+        datlas = resident.cached(
+            "perprim", scene, dkey + (smp, texel_format), resident.scene_arrays(scene)[6:],
+            lambda: DeviceAtlas(texels=scene_texels(scene), linear=(smp == "verify"),
+                                hw=(smp == "hw"), texel_format=texel_format, device=device))
     else:
         if atlas_set is None:
             raise ValueError("atlas mode needs a packed atlas_set")
@@ -185,8 +205,10 @@ def prepare(scene, camera=None, texture_mode: str = "perprim", atlas_set=None, *
         else:
             if atlas_set.resolution != T:
                 raise ValueError("atlas resolution mismatch with scene")
-            datlas = DeviceAtlas(atlas_set, linear=(smp == "verify"), hw=(smp == "hw"),
-                                 texel_format=texel_format, device=device)
+            datlas = resident.cached(
+                "atlas", atlas_set, dkey + (smp, texel_format), resident.atlas_arrays(atlas_set),
+                lambda: DeviceAtlas(atlas_set, linear=(smp == "verify"), hw=(smp == "hw"),
+                                    texel_format=texel_format, device=device))
         if datlas.resolution != T:
             raise ValueError("atlas resolution mismatch with scene")
     if texture_mode != "flat" and datlas.num_entries < dscene.num_splats:
@@ -207,9 +229,7 @@ def render_prepared(prep: PreparedScene, camera, tile: int = TILE, *, out=None,
     ws = prep.workspace
     if ws.key != (P, W, H, tile):
         ws.ensure(P, W, H, tile, FrameWorkspace.initial_capacity(P, W, H, tile))
-    elif getattr(ws, "shrink_to", None):
-        ws.ensure(P, W, H, tile, ws.shrink_to, exact=True)
-        ws.shrink_to = None
+    ws.generation += 1
     gbuf = out if out is not None else torch.empty((NUM_CHANNELS, H, W), dtype=torch.float32,
                                                    device=dev)
     px = pixels if pixels is not None else PixelState.empty(H, W, dev)
@@ -228,13 +248,11 @@ def render_prepared(prep: PreparedScene, camera, tile: int = TILE, *, out=None,
             break
         needed = int(ws.needed.item())
         if needed <= ws.capacity:
-            # the binning sorts the whole capacity: shrink a generous first
-            # guess for the next frames (this frame's tape keeps its buffer)
-            if ws.capacity > 2 * needed + 65536:
-                ws.shrink_to = int(needed * 1.25) + 4096
             break
         ws.ensure(P, W, H, tile, int(needed * 1.25) + 1024)
-    tape = Tape(prep, camera, tile, ws.capacity, ws.buf, ws.nbytes, px, gbuf, mode)
+        ws.generation += 1
+    tape = Tape(prep, camera, tile, ws.capacity, ws.buf, ws.nbytes, px, gbuf, mode,
+                generation=ws.generation)
     return GBuffer(gbuf, px), tape
 
 
@@ -250,6 +268,14 @@ def render_forward(scene, camera, texture_mode: str = "perprim", atlas_set=None,
     if prep is None:
         prep = prepare(scene, camera, texture_mode, atlas_set, sampler=sampler,
                        texel_format=texel_format)
+        if not with_tape:
+            # no tape outlives the call: the scene's cached workspace serves
+            # every such frame (a tape gets its own, as the reference's tapes
+            # are independent objects)
+            shared = getattr(prep.scene, "_shared_workspace", None)
+            if shared is None:
+                shared = prep.scene._shared_workspace = prep.workspace
+            prep.workspace = shared
     gbuf, tape = render_prepared(prep, camera, tile)
     return (gbuf, tape) if with_tape else gbuf
 

@@ -14,7 +14,7 @@ import ctypes as C
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, resident
 from .device import DeviceAtlas, DeviceEnvironment, DeviceScene, FrameWorkspace
 from .rasterize import NUM_CHANNELS, TILE, GBuffer, PixelState, PreparedScene, prepare, render_prepared
 from .shading import ShadeResult, shade_planar
@@ -36,7 +36,7 @@ class Renderer:
             raise ValueError("Renderer needs an environment")
         if lut is None and not isinstance(env, DeviceEnvironment):
             from .environment import BrdfLut
-            lut = BrdfLut.build()
+            lut = BrdfLut.build(device=self.prep.scene.device)  # K16 on the GPU
         self.env = env if isinstance(env, DeviceEnvironment) else DeviceEnvironment(
             env, lut, self.prep.scene.device)
         self.tile = tile
@@ -64,14 +64,33 @@ class Renderer:
         return self._bufs[key]
 
     def reserve(self, camera, entries: int):
-        """Pre-size the frame workspace (no per-frame capacity sync needed)."""
+        """Pre-size the frame workspace (no per-frame capacity sync needed).
+        Frames replayed with check=False are validated afterwards with
+        check_capacity() (or automatically by stream_views)."""
         ws = self.prep.workspace
         ws.ensure(self.prep.scene.num_splats, int(camera.width), int(camera.height), self.tile,
                   entries, exact=True)
-        ws.shrink_to = None
 
     def entries_needed(self) -> int:
+        """Entry count of the last binned frame."""
         return int(self.prep.workspace.needed.item())
+
+    def max_entries_needed(self) -> int:
+        """Largest entry count of any frame since the last reset (host sync)."""
+        return self.prep.workspace.max_needed_value()
+
+    def check_capacity(self, reset: bool = True):
+        """Raise if any frame rendered since the last check outgrew the
+        workspace (such a frame has empty tile lists: background only). The
+        running maximum lives on the device (k_ranges), so graph replays need
+        no per-frame host sync."""
+        ws = self.prep.workspace
+        need = ws.max_needed_value()
+        if reset:
+            ws.reset_max()
+        if need > ws.capacity:
+            raise RuntimeError(f"frame workspace overflow: a frame needed {need} tile entries, "
+                               f"capacity {ws.capacity}; reserve() more and re-render")
 
     def _graph(self, camera, W, H, binned_event=None):
         """CUDA graph of this view size over the current buffers (rebuilt if
@@ -154,8 +173,32 @@ class Renderer:
         lists are built (an event recorded inside the frame graph), so it
         overlaps frame i+1's rasteriser rather than its latency-bound
         binning. Yields (index, host colour tensor) in order as each copy
-        completes; a host buffer is reused `depth` frames later."""
+        completes; a host buffer is reused `depth` frames later.
+
+        Capacity: with every image the device's running maximum of the
+        frames' entry counts comes back too. A frame is yielded only once it
+        is known to have fitted the workspace; on an overflow the workspace
+        grows and the stream resumes from the first unverified frame."""
         cams = list(cameras)
+        start = 0
+        while start < len(cams):
+            resume = None
+            for i, img in self._stream(cams[start:], host_out, depth):
+                if img is None:       # overflow detected: frames >= i unverified
+                    resume = start + i
+                    break
+                yield start + i, img
+            if resume is None:
+                return
+            torch.cuda.current_stream(self.device).synchronize()
+            ws = self.prep.workspace
+            need = ws.max_needed_value()
+            c = cams[resume]
+            ws.ensure(self.prep.scene.num_splats, int(c.width), int(c.height), self.tile,
+                      int(need * 1.25) + 4096)
+            start = resume
+
+    def _stream(self, cams, host_out, depth):
         if not cams:
             return
         W, H = int(cams[0].width), int(cams[0].height)
@@ -169,20 +212,39 @@ class Renderer:
                 [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(depth)],
                 [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True)
                  for _ in range(depth)],
-                torch.cuda.Stream(dev), binned)
-        dcol, hcol_cached, copy, binned = self._bufs[key]
+                torch.cuda.Stream(dev), binned,
+                torch.zeros((depth,), dtype=torch.int64, pin_memory=True))
+        dcol, hcol_cached, copy, binned, hmax = self._bufs[key]
         hcol = host_out or hcol_cached
+        ws = self.prep.workspace
         compute = torch.cuda.current_stream(dev)
         done = [torch.cuda.Event() for _ in range(depth)]
         ready = torch.cuda.Event()
         use_ev = self._graph_ready(W, H)
+        if ws.max_needed is not None:
+            ws.reset_max()            # (on the compute stream, before the first frame)
+        verified = -1                 # frames <= verified fitted the workspace
 
         def queue_copy(j, after):
             b = j % depth
             copy.wait_event(after)
             with torch.cuda.stream(copy):
                 hcol[b].copy_(dcol[b], non_blocking=True)
+                if ws.max_needed is not None:  # running max incl. the frames binned so far
+                    hmax[b:b + 1].copy_(ws.max_needed, non_blocking=True)
             done[b].record(copy)
+
+        def emit(j):
+            """(j, image) if frame j is known to fit, else (j, None)."""
+            nonlocal verified
+            b = j % depth
+            done[b].synchronize()
+            if ws.max_needed is None or int(hmax[b]) <= ws.capacity:
+                # this read covers every frame binned before the copy started:
+                # frame j + 1 too, except for the last frame
+                verified = max(verified, j + 1 if j + 1 < len(cams) else j)
+                return j, hcol[b]
+            return j, (hcol[b] if j <= verified else None)
 
         for i, cam in enumerate(cams):
             b = i % depth
@@ -197,14 +259,24 @@ class Renderer:
                     ready.record(compute)       # no graph: after frame i
                     queue_copy(i - 1, ready)
             if i >= 2:
-                done[(i - 2) % depth].synchronize()
-                yield i - 2, hcol[(i - 2) % depth]
+                j, img = emit(i - 2)
+                yield j, img
+                if img is None:
+                    return
+                if j + 1 > verified:            # the next frame is already known bad
+                    yield j + 1, None
+                    return
         n = len(cams)
         ready.record(compute)
         queue_copy(n - 1, ready)
         for j in range(max(0, n - 2), n):
-            done[j % depth].synchronize()
-            yield j, hcol[j % depth]
+            jj, img = emit(j)
+            yield jj, img
+            if img is None:
+                return
+            if jj + 1 < n and jj + 1 > verified:
+                yield jj + 1, None
+                return
 
     def shade(self, gbuf: GBuffer, camera) -> ShadeResult:
         c, d, s = shade_planar(gbuf.planar, camera, self.env, self.background)
@@ -220,6 +292,15 @@ def render(camera, gaussians, atlas=None, envmap=None, lut=None, background=None
     """
     texture_mode = "flat" if mode == "flat" else "atlas"
     sampler = None if mode == "flat" else mode
-    r = Renderer(gaussians, atlas, envmap, lut, texture_mode=texture_mode, sampler=sampler,
-                 tile=tile, background=background)
+    env = envmap if envmap is not None else getattr(gaussians, "environment", None)
+    # one Renderer per (scene, atlas, environment, LUT) objects (resident.py):
+    # repeated calls re-upload nothing and reuse the frame workspace
+    key = (id(atlas), id(env), id(lut), mode, tile, None if background is None
+           else tuple(float(v) for v in np.asarray(background, np.float64)))
+    r = resident.cached(
+        "renderer", gaussians, key,
+        resident.scene_arrays(gaussians) + resident.env_arrays(env, lut)
+        + (resident.atlas_arrays(atlas) if atlas is not None else []),
+        lambda: Renderer(gaussians, atlas, envmap, lut, texture_mode=texture_mode,
+                         sampler=sampler, tile=tile, background=background))
     return r.render(camera)

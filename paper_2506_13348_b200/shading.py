@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, resident
 from .device import DeviceEnvironment
 
 COS_MIN = 1e-4
@@ -35,11 +35,13 @@ class ShadeResult:
 
 
 def device_environment(env, lut, device=None) -> DeviceEnvironment:
+    """The environment + LUT in HBM, cached per (env, lut) host objects."""
     if isinstance(env, DeviceEnvironment):
         return env
     if env is None:
         raise ValueError("shading needs an environment")
-    return DeviceEnvironment(env, lut, device)
+    return resident.cached("env", env, (id(lut), str(device)), resident.env_arrays(env, lut),
+                           lambda: DeviceEnvironment(env, lut, device))
 
 
 def shade_planar(planar: torch.Tensor, camera, denv: DeviceEnvironment, background=None, *,
