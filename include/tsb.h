@@ -272,6 +272,25 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera,
                         const tsb_pixel_state* pixels, const float* dgbuf, void* scratch,
                         tsb_scene_grads* grads, void* stream);
 
+/* tsb_render_backward with a `deterministic` switch: the
+ * reference reduces in a fixed tile order (rasterize.py:494, :646), so its
+ * gradients are repeatable; the default path accumulates with float atomics
+ * (order-dependent low bits). deterministic != 0 accumulates the per-splat
+ * terms and texel gradients as int64 fixed point (2^-32 / 2^-40 resolution;
+ * integer adds commute), so two runs give bitwise-equal gradients.
+ * det_scratch: tsb_backward_det_scratch_size bytes (ignored otherwise). */
+int tsb_render_backward_ex(const tsb_scene* scene, const tsb_camera* camera,
+                           const tsb_atlas* atlas, int32_t tile, const void* workspace,
+                           uint64_t workspace_bytes, int64_t max_entries,
+                           const tsb_pixel_state* pixels, const float* dgbuf, void* scratch,
+                           tsb_scene_grads* grads, int32_t deterministic, void* det_scratch,
+                           uint64_t det_scratch_bytes, void* stream);
+
+/* Scratch bytes of the deterministic backward for P splats at T x T texels
+ * in `texel_layout` (TSB_TEXELS_COMBINED / TSB_TEXELS_INTERLEAVED). */
+int tsb_backward_det_scratch_size(int32_t num_splats, int32_t T, int32_t texel_layout,
+                                  uint64_t* bytes);
+
 /* ---- Training-step glue (K10-K13) ------------------------------------- */
 
 /* Scratch bytes of tsb_loss_image for a W x H image. */

@@ -114,7 +114,11 @@ _SIGNATURES = {
     "tsb_render_backward": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
                             C.c_int32, _P, C.c_uint64, C.c_int64, C.POINTER(PixelState_t), _P,
                             _P, C.POINTER(SceneGrads_t), _P],
+    "tsb_render_backward_ex": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
+                               C.c_int32, _P, C.c_uint64, C.c_int64, C.POINTER(PixelState_t),
+                               _P, _P, C.POINTER(SceneGrads_t), C.c_int32, _P, C.c_uint64, _P],
     "tsb_backward_scratch_size": [C.c_int32, C.POINTER(C.c_uint64)],
+    "tsb_backward_det_scratch_size": [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)],
     "tsb_loss_scratch_size": [C.c_int32, C.c_int32, C.POINTER(C.c_uint64)],
     "tsb_loss_image": [_P, _P, C.c_int32, C.c_int32, C.c_float, _P, _P, _P, C.c_uint64, _P],
     "tsb_loss_regularizers": [_P, _P, C.POINTER(Camera_t), C.c_float, C.c_float, _P, _P, _P],

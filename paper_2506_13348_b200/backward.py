@@ -86,13 +86,16 @@ def _planar(dbuf, H, W, device) -> torch.Tensor:
 
 
 def splat_backward(scene, camera, prep, tape: Tape, dbuf, *, grads: SceneGrads = None,
-                   scratch: torch.Tensor = None) -> SceneGrads:
+                   scratch: torch.Tensor = None, deterministic: bool = False) -> SceneGrads:
     """Backpropagate a G-buffer gradient to splat parameters.
 
     `tape` is the second return of render_forward(..., with_tape=True) in
     texture_mode "perprim" (fp32 software sampling), as in the reference
     (rasterize.py:482-483 raises ValueError otherwise). `scene` and `prep`
     are accepted for signature parity; the frame state lives in the tape.
+    deterministic=True: bitwise-repeatable gradients (int64 fixed-point
+    accumulation, tsb_render_backward_ex) like the reference's fixed-order
+    reduction (rasterize.py:494, :646); the default float atomics are faster.
     """
     del scene
     if tape.mode != _lib.MODE_VERIFY or tape.prep.texture_mode == "flat":
@@ -116,10 +119,18 @@ def splat_backward(scene, camera, prep, tape: Tape, dbuf, *, grads: SceneGrads =
     sc, at, cam = ds.struct(), prep.atlas.struct(), _lib.camera_struct(camera)
     pst = tape.pixels.struct()
     gs = grads.struct()
-    _lib.check(L.tsb_render_backward(C.byref(sc), C.byref(cam), C.byref(at), tape.tile,
-                                     _lib.ptr(tape.workspace), tape.workspace_bytes,
-                                     tape.capacity, C.byref(pst), _lib.ptr(dplanar),
-                                     _lib.ptr(scratch), C.byref(gs), _lib.stream_handle()),
+    det = None
+    if deterministic:
+        nb = C.c_uint64()
+        _lib.check(L.tsb_backward_det_scratch_size(P, T, grads.texel_layout, C.byref(nb)),
+                   "tsb_backward_det_scratch_size")
+        det = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
+    _lib.check(L.tsb_render_backward_ex(C.byref(sc), C.byref(cam), C.byref(at), tape.tile,
+                                        _lib.ptr(tape.workspace), tape.workspace_bytes,
+                                        tape.capacity, C.byref(pst), _lib.ptr(dplanar),
+                                        _lib.ptr(scratch), C.byref(gs), 1 if deterministic else 0,
+                                        _lib.ptr(det), 0 if det is None else det.numel(),
+                                        _lib.stream_handle()),
                "tsb_render_backward")
     return grads
 

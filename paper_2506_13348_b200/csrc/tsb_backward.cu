@@ -34,6 +34,15 @@
 namespace tsb {
 
 constexpr int kAccWords = 24;  // per-splat accumulator stride (22 used)
+// Deterministic backward: fixed-point scales of the int64 accumulators.
+// Per-splat terms: resolution 2^-32 (2.3e-10), range +-2^31; texel
+// gradients: resolution 2^-40 (9.1e-13), range +-2^23. Each contribution is
+// rounded to the grid once; the sums are then exact, so bitwise repeatable.
+constexpr int kAccFix = 32, kTexFix = 40;
+
+__device__ __forceinline__ unsigned long long to_fix(float v, int shift) {
+  return (unsigned long long)__double2ll_rn((double)v * (double)(1ull << shift));
+}
 // accumulator layout: [0..9) dWH rows 0..2 x cols (0,1,3); [9] dopacity;
 // [10..13) dl_ind; [13..16) dframe_u; [16..19) dframe_v; [19..22) dn3.
 
@@ -345,6 +354,10 @@ struct RasterBwdParams {
   const float* dgbuf;
   float* acc;          // P x kAccWords
   float* dtexels;      // P x T x T x tl
+  // deterministic mode: fixed-point int64 accumulators instead of the float
+  // atomics above (integer adds commute, so any order gives the same bits)
+  unsigned long long* acc64;  // P x kAccWords, value * 2^kAccFix
+  unsigned long long* tex64;  // P x T x T x tl, value * 2^kTexFix
   int32_t tl;          // channels per texel: 7 (combined) or 8 (interleaved)
   int32_t num_tiles;
   int32_t* work_counter;
@@ -387,6 +400,7 @@ __device__ __forceinline__ void decode_grad(float ea, float eb, float gx, float 
   denc[1] = 2.0f * dpy;
 }
 
+template <bool DET>
 __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -636,7 +650,12 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
           const int nl = __popc(lm);
           float tot = 0.f;
           for (int i = 0; i < nl; ++i) tot += ws.red[28 * i + lane];
-          if (tot != 0.0f) atomicAdd(p.acc + (size_t)kAccWords * id + lane, tot);
+          if (tot != 0.0f) {
+            if constexpr (DET)
+              atomicAdd(p.acc64 + (size_t)kAccWords * id + lane, to_fix(tot, kAccFix));
+            else
+              atomicAdd(p.acc + (size_t)kAccWords * id + lane, tot);
+          }
         }
         __syncwarp();
         if (lk) {
@@ -664,13 +683,33 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
               for (uint32_t m = grp; m; m &= m - 1) tsum += ws.red[36 * (__ffs(m) - 1) + lane];
               const int* lr = reinterpret_cast<const int*>(ws.red + 36 * l + 28);
               const int off = lr[0] + ((t_corner & 1) ? lr[1] : 0) + ((t_corner & 2) ? lr[2] : 0) + t_slot;
-              if (tsum != 0.0f) atomicAdd(dt + off, tsum);
+              if (tsum != 0.0f) {
+                if constexpr (DET)
+                  atomicAdd(p.tex64 + (size_t)id * T * T * tl + off, to_fix(tsum, kTexFix));
+                else
+                  atomicAdd(dt + off, tsum);
+              }
             }
           }
         }
         __syncwarp();
       }
     }
+  }
+}
+
+// Deterministic mode: fixed-point sums back to float (texel gradients are
+// ADDED to the caller's buffer, like the atomic path).
+__global__ void k_det_unfix(int64_t n_acc, const unsigned long long* __restrict__ acc64,
+                            float* __restrict__ acc, int64_t n_tex,
+                            const unsigned long long* __restrict__ tex64,
+                            float* __restrict__ dtexels) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_acc; i += stride)
+    acc[i] = (float)((double)(long long)acc64[i] * (1.0 / (double)(1ull << kAccFix)));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_tex; i += stride) {
+    const long long v = (long long)tex64[i];
+    if (v) dtexels[i] += (float)((double)v * (1.0 / (double)(1ull << kTexFix)));
   }
 }
 
@@ -837,6 +876,18 @@ int tsb_backward_scratch_size(int32_t P, uint64_t* bytes) {
   return TSB_OK;
 }
 
+int tsb_backward_det_scratch_size(int32_t P, int32_t T, int32_t texel_layout, uint64_t* bytes) {
+  if (!bytes || P < 0 || T < 1 ||
+      (texel_layout != TSB_TEXELS_COMBINED && texel_layout != TSB_TEXELS_INTERLEAVED)) {
+    set_error("tsb_backward_det_scratch_size: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  const uint64_t Pn = (uint64_t)(P > 0 ? P : 1);
+  const uint64_t tl = texel_layout == TSB_TEXELS_INTERLEAVED ? 8 : 7;
+  *bytes = Pn * kAccWords * 8 + Pn * (uint64_t)T * T * tl * 8;
+  return TSB_OK;
+}
+
 // Floats of all environment grids at `ch` floats per texel (offsets per grid).
 static int32_t env_floats(const tsb_environment* env, int32_t* off, int ch = 3) {
   int32_t o = 0;
@@ -917,9 +968,30 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera, const 
                         int32_t tile, const void* ws, uint64_t ws_bytes, int64_t cap,
                         const tsb_pixel_state* px, const float* dgbuf, void* scratch,
                         tsb_scene_grads* grads, void* stream) {
+  return tsb_render_backward_ex(scene, camera, atlas, tile, ws, ws_bytes, cap, px, dgbuf, scratch,
+                                grads, 0, nullptr, 0, stream);
+}
+
+int tsb_render_backward_ex(const tsb_scene* scene, const tsb_camera* camera,
+                           const tsb_atlas* atlas, int32_t tile, const void* ws,
+                           uint64_t ws_bytes, int64_t cap, const tsb_pixel_state* px,
+                           const float* dgbuf, void* scratch, tsb_scene_grads* grads,
+                           int32_t deterministic, void* det_scratch, uint64_t det_scratch_bytes,
+                           void* stream) {
   if (!scene || !camera || !atlas || !ws || !px || !dgbuf || !scratch || !grads) {
     set_error("tsb_render_backward: null argument");
     return TSB_ERR_VALUE;
+  }
+  if (deterministic) {
+    uint64_t need = 0;
+    const int rc = tsb_backward_det_scratch_size(scene->num_splats, atlas->resolution,
+                                                 grads->texel_layout, &need);
+    if (rc != TSB_OK) return rc;
+    if (!det_scratch || det_scratch_bytes < need) {
+      set_error("tsb_render_backward: deterministic mode needs tsb_backward_det_scratch_size "
+                "bytes of det_scratch");
+      return TSB_ERR_CAPACITY;
+    }
   }
   if (!atlas->family_a || !atlas->family_b || !atlas->entries) {
     set_error("gradients require the per-primitive (linear atlas) texture path");
@@ -958,6 +1030,12 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera, const 
   rp.acc = acc;
   rp.dtexels = grads->texels;
   rp.tl = grads->texel_layout == TSB_TEXELS_INTERLEAVED ? 8 : 7;
+  const int64_t n_acc = (int64_t)P * kAccWords;
+  const int64_t n_tex = (int64_t)P * atlas->resolution * atlas->resolution * rp.tl;
+  rp.acc64 = deterministic ? static_cast<unsigned long long*>(det_scratch) : nullptr;
+  rp.tex64 = deterministic ? rp.acc64 + n_acc : nullptr;
+  if (deterministic)
+    TSB_CUDA(cudaMemsetAsync(det_scratch, 0, (size_t)(n_acc + n_tex) * 8, st));
   rp.num_tiles = L.num_tiles;
   rp.work_counter = reinterpret_cast<int32_t*>(const_cast<int64_t*>(ws_ptr<int64_t>(ws, L.counters)) + 2);
   rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);
@@ -968,17 +1046,29 @@ int tsb_render_backward(const tsb_scene* scene, const tsb_camera* camera, const 
   TSB_CUDA(s_resident.get(
       [smem](int dev) {
         int sms = 0, per_sm = 0;
-        cudaError_t e = cudaFuncSetAttribute(k_raster_bwd,
+        cudaError_t e = cudaFuncSetAttribute(k_raster_bwd<false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(k_raster_bwd<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (e == cudaSuccess)
-          e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_bwd, 256, smem);
+          e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_bwd<false>, 256,
+                                                            smem);
         return e == cudaSuccess ? sms * (per_sm > 0 ? per_sm : 1) : -(int)e;
       },
       &resident));
   const int units = L.num_tiles * (tile * tile / 32);
-  k_raster_bwd<<<std::min((units + 7) / 8, resident), 256, smem, st>>>(rp);
-  TSB_CHECK_LAUNCH("k_raster_bwd");
+  const int grid = std::min((units + 7) / 8, resident);
+  if (deterministic) {
+    k_raster_bwd<true><<<grid, 256, smem, st>>>(rp);
+    TSB_CHECK_LAUNCH("k_raster_bwd<det>");
+    k_det_unfix<<<1184, 256, 0, st>>>(n_acc, rp.acc64, acc, n_tex, rp.tex64, rp.dtexels);
+    TSB_CHECK_LAUNCH("k_det_unfix");
+  } else {
+    k_raster_bwd<false><<<grid, 256, smem, st>>>(rp);
+    TSB_CHECK_LAUNCH("k_raster_bwd");
+  }
   FinishParams fp;
   fp.cam = to_cam(camera);
   fp.P = P; fp.sh_degree = scene->sh_degree;

@@ -129,3 +129,39 @@ def test_data_parallel_trainer_reduces_loss():
     losses = [tr.step(cam, tgt)[0]["loss"] for _ in range(20)]
     assert all(np.isfinite(losses))
     assert max(losses[-5:]) < 0.8 * losses[0], losses
+
+
+def test_deterministic_backward_is_bitwise_repeatable():
+    """tsb_render_backward_ex(deterministic=1): int64 fixed-point sums, so two
+    runs agree bit for bit (the float-atomic default need not), and both
+    modes agree with each other and with the reference's gradients."""
+    g = gio.load("backward")
+    scene, cam = gio.scene(g, "gc_"), gio.camera(g, "gc_cam_")
+    gbuf, tape = render_forward(scene, cam, "perprim", with_tape=True)
+    a = splat_backward(scene, cam, None, tape, g["gc_dgbuf"], deterministic=True)
+    b = splat_backward(scene, cam, None, tape, g["gc_dgbuf"], deterministic=True)
+    for x, y in zip(a.flat(), b.flat()):
+        assert torch.equal(x, y)
+    _grads_vs(g, "gc_", a)
+    f = splat_backward(scene, cam, None, tape, g["gc_dgbuf"])
+    for x, y in zip(a.flat(), f.flat()):
+        scale = float(y.abs().max()) if y.numel() else 0.0
+        assert float((x - y).abs().max()) <= 1e-4 * scale + 1e-9
+
+
+def test_deterministic_backward_at_cfg4_scale():
+    """The same on an 80x80 window of the 100k-splat cfg4 scene (real list
+    lengths, many warps adding into the same splats and texels)."""
+    gc_ = gio.load("train_crop")
+    scene = gio.cfg2_scene()
+    cam = gio.camera(gc_)
+    dbuf = np.random.default_rng(7).normal(size=(cam.height, cam.width, 13))
+    gbuf, tape = render_forward(scene, cam, "perprim", with_tape=True)
+    runs = [splat_backward(scene, cam, None, tape, dbuf, deterministic=True) for _ in range(3)]
+    for r in runs[1:]:
+        for x, y in zip(runs[0].flat(), r.flat()):
+            assert torch.equal(x, y)
+    f = splat_backward(scene, cam, None, tape, dbuf)
+    for x, y in zip(runs[0].flat(), f.flat()):
+        scale = float(y.abs().max()) if y.numel() else 0.0
+        assert float((x - y).abs().max()) <= 1e-4 * scale + 1e-9
