@@ -326,6 +326,9 @@ int tsb_loss_regularizers(const float* gbuf, const float* target, const tsb_came
 #define TSB_ADAM_MAX_GROUPS 24
 #define TSB_F32 0
 #define TSB_F64 1
+/* float32 texels in the 8-channel interleaved order (count = P*T*T*8) with
+ * float32 gradients in the 7-channel combined order (P*T*T*7) */
+#define TSB_F32_TEX87 2
 #define TSB_CLAMP_NONE 0
 #define TSB_CLAMP_UNIT 1
 #define TSB_CLAMP_FLOOR 2
@@ -343,10 +346,45 @@ typedef struct tsb_adam_group {
 int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step, double beta1,
                   double beta2, double eps, void* stream);
 
+/* K12 with a divergence guard: no update when *halt != 0 (device int32, set
+ * by tsb_guard_finite), so a diverged step leaves the parameters as the
+ * reference's train() leaves them when it raises (training.py:263-265). */
+int tsb_adam_step_ex(const tsb_adam_group* groups, int32_t num_groups, int32_t step,
+                     double beta1, double beta2, double eps, const int32_t* halt, void* stream);
+
 /* K13: Gram-Schmidt re-orthonormalisation of the tangent frames
  * (Scene.renormalize_tangents, splats.py:382-392), in place, float64. */
 int tsb_orthonormalize_tangents(int32_t num_splats, double* tangent_u, double* tangent_v,
                                 void* stream);
+int tsb_orthonormalize_tangents_ex(int32_t num_splats, double* tangent_u, double* tangent_v,
+                                   const int32_t* halt, void* stream);
+
+/* ---- train() loop glue (training.py:187-322) -------------------------- */
+
+/* Sets *halt = 1 if any of terms[0..n) is not finite (the loss guard of
+ * training.py:263-265, evaluated on the device: no host sync per step). */
+int tsb_guard_finite(const double* terms, int32_t n, int32_t* halt, void* stream);
+
+/* Stage-2 chart growth (broadcast_textures, training.py:201-221) of texels in
+ * the 8-channel interleaved (P, T, T, 8) float32 layout: T0 x T0 -> T x T,
+ * each texel repeated T/T0 times per axis (or texel (0,0) repeated when T is
+ * not a multiple of T0). src and dst must not overlap. */
+int tsb_broadcast_texels(int32_t num_splats, int32_t T0, int32_t T, const float* src, float* dst,
+                         void* stream);
+
+/* Opacity pruning (_prune, training.py:187-198): keeps, in order, the rows
+ * whose opacity > threshold, gathering each buffer's rows from src into dst
+ * (parameters, texels, Adam moments: any row size); *kept (device int32)
+ * receives the kept count. scratch: tsb_prune_scratch_size bytes. */
+typedef struct tsb_row_buffer {
+  const void* src;
+  void* dst;
+  int64_t row_bytes;
+} tsb_row_buffer;
+int tsb_prune_scratch_size(int32_t num_splats, uint64_t* bytes);
+int tsb_prune_rows(int32_t num_splats, const double* opacities, double threshold,
+                   const tsb_row_buffer* bufs, int32_t num_bufs, int32_t* kept, void* scratch,
+                   uint64_t scratch_bytes, void* stream);
 
 /* ---- Environment precompute (K15-K17) ---------------------------------- */
 

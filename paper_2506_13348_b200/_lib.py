@@ -73,8 +73,12 @@ TEXELS_COMBINED = 0
 TEXELS_INTERLEAVED = 1
 
 ADAM_MAX_GROUPS = 24
-F32, F64 = 0, 1
+F32, F64, F32_TEX87 = 0, 1, 2
 CLAMP_NONE, CLAMP_UNIT, CLAMP_FLOOR = 0, 1, 2
+
+
+class RowBuffer_t(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("row_bytes", C.c_int64)]
 
 
 class AdamGroup_t(C.Structure):
@@ -125,6 +129,14 @@ _SIGNATURES = {
     "tsb_adam_step": [C.POINTER(AdamGroup_t), C.c_int32, C.c_int32, C.c_double, C.c_double,
                       C.c_double, _P],
     "tsb_orthonormalize_tangents": [C.c_int32, _P, _P, _P],
+    "tsb_orthonormalize_tangents_ex": [C.c_int32, _P, _P, _P, _P],
+    "tsb_adam_step_ex": [C.POINTER(AdamGroup_t), C.c_int32, C.c_int32, C.c_double, C.c_double,
+                         C.c_double, _P, _P],
+    "tsb_guard_finite": [_P, C.c_int32, _P, _P],
+    "tsb_broadcast_texels": [C.c_int32, C.c_int32, C.c_int32, _P, _P, _P],
+    "tsb_prune_scratch_size": [C.c_int32, C.POINTER(C.c_uint64)],
+    "tsb_prune_rows": [C.c_int32, _P, C.c_double, C.POINTER(RowBuffer_t), C.c_int32, _P, _P,
+                       C.c_uint64, _P],
     "tsb_frame_graph_create": [C.POINTER(Scene_t), C.POINTER(Camera_t), C.POINTER(Atlas_t),
                                C.c_int32, C.c_int32, _P, C.c_uint64, C.c_int64, _P,
                                C.POINTER(PixelState_t), _P, C.POINTER(Environment_t), _P, _P,

@@ -494,6 +494,7 @@ struct AdamLaunch {
   int32_t n;
   double b1, b2, eps;
   double bc1, bc2;  // 1 - beta^t
+  const int32_t* halt;  // optional: skip the update when *halt != 0 (divergence guard)
 };
 
 template <typename TP>
@@ -558,12 +559,44 @@ __device__ __forceinline__ void adam_chunk_f4(const AdamLaunch& A, const tsb_ada
 
 // One block = one contiguous chunk of one group (coalesced, no per-element
 // group search).
+// Texels as parameters in the 8-channel interleaved atlas order (what the
+// verify-mode forward reads) with gradients in the 7-channel combined order
+// (what K8 writes with TSB_TEXELS_COMBINED, and what the all-reduce carries:
+// no always-zero 8th channel on the wire). Slot -> combined channel; the pad
+// slot 7 stays untouched.
+__device__ __forceinline__ void adam_chunk_tex87(const AdamLaunch& A, const tsb_adam_group& g,
+                                                 int64_t base) {
+  float* prm = static_cast<float*>(g.param);
+  float* m = static_cast<float*>(g.m);
+  float* v = static_cast<float*>(g.v);
+  const float b1 = (float)A.b1, b2 = (float)A.b2, c1 = (float)(1.0 - A.b1), c2 = (float)(1.0 - A.b2);
+  const float ibc1 = (float)(1.0 / A.bc1), ibc2 = (float)(1.0 / A.bc2), lr = (float)g.lr;
+  const float eps = (float)A.eps;
+  constexpr int kSlotToCombined[8] = {0, 1, 2, 3, 5, 6, 4, -1};
+#pragma unroll 4
+  for (int j = 0; j < kAdamChunk / 256; ++j) {
+    const int64_t i = base + j * 256 + threadIdx.x;
+    if (i >= g.count) break;
+    const int slot = (int)(i & 7);
+    const int c = kSlotToCombined[slot];
+    if (c < 0) continue;
+    const float gr = __ldg(g.grad + (i >> 3) * 7 + c);
+    float mi = m[i], vi = v[i];
+    prm[i] = adam_f(prm[i], gr, mi, vi, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+    m[i] = mi;
+    v[i] = vi;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_adam(AdamLaunch A) {
+  if (A.halt && *A.halt) return;
   int k = 0;
   while (k + 1 < A.n && A.blk_start[k + 1] <= (int)blockIdx.x) ++k;
   const tsb_adam_group& g = A.g[k];
   const int64_t base = (int64_t)(blockIdx.x - A.blk_start[k]) * kAdamChunk;
-  if (g.dtype == TSB_F64) {
+  if (g.dtype == TSB_F32_TEX87) {
+    adam_chunk_tex87(A, g, base);
+  } else if (g.dtype == TSB_F64) {
     adam_chunk<double>(A, g, base);
   } else if ((g.count & 3) == 0 && ((reinterpret_cast<uintptr_t>(g.param) |
                                      reinterpret_cast<uintptr_t>(g.m) |
@@ -576,9 +609,10 @@ __global__ void __launch_bounds__(256) k_adam(AdamLaunch A) {
 }
 
 // ---- K13 tangent frames ------------------------------------------------------
-__global__ void k_orthonormalize(int32_t P, double* __restrict__ tu, double* __restrict__ tv) {
+__global__ void k_orthonormalize(int32_t P, double* __restrict__ tu, double* __restrict__ tv,
+                                 const int32_t* __restrict__ halt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
+  if (i >= P || (halt && *halt)) return;
   double u[3], v[3];
   for (int k = 0; k < 3; ++k) { u[k] = tu[3 * i + k]; v[k] = tv[3 * i + k]; }
   const double nu = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
@@ -587,6 +621,96 @@ __global__ void k_orthonormalize(int32_t P, double* __restrict__ tu, double* __r
   for (int k = 0; k < 3; ++k) v[k] = v[k] - d * u[k];
   const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
   for (int k = 0; k < 3; ++k) { tu[3 * i + k] = u[k]; tv[3 * i + k] = v[k] / nv; }
+}
+
+// ---- train loop glue (train(), training.py:224-322) ------------------------
+// Divergence guard (training.py:263-265): halt = 1 once any loss term of a
+// step is non-finite; the guarded Adam / orthonormalisation then skip, so the
+// parameters stay those of the iteration that diverged (the reference raises
+// before updating) while the host reads the flag at its next sync.
+__global__ void k_guard_finite(const double* __restrict__ terms, int32_t n,
+                               int32_t* __restrict__ halt) {
+  const int i = threadIdx.x;
+  if (i < n && !isfinite(terms[i])) *halt = 1;
+}
+
+// Stage-2 texel broadcast (broadcast_textures, training.py:201-221): charts of
+// T0 x T0 texels grow to T x T by repeating each texel T/T0 times per axis,
+// or (T not a multiple of T0) by repeating texel (0, 0). 8-channel layout.
+__global__ void k_broadcast_texels(int64_t P, int32_t T0, int32_t T, const float4* __restrict__ src,
+                                   float4* __restrict__ dst) {
+  const int64_t n = P * T * T;
+  const bool even = T % T0 == 0;
+  const int reps = even ? T / T0 : 1;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = q / ((int64_t)T * T);
+    const int r = (int)(q % ((int64_t)T * T));
+    const int j = r / T, i = r % T;
+    const int64_t s = even ? p * T0 * T0 + (int64_t)(j / reps) * T0 + i / reps : p * T0 * T0;
+    dst[2 * q] = src[2 * s];
+    dst[2 * q + 1] = src[2 * s + 1];
+  }
+}
+
+// Opacity pruning (_prune, training.py:187-198): rows with opacity > threshold
+// are kept, in order, in every listed buffer (parameters, texels, Adam
+// moments). Three launches: per-block keep counts, one CTA scanning them,
+// then a stable gather of every buffer's rows.
+constexpr int kPruneBlock = 1024;
+
+__global__ void k_prune_count(int32_t P, const double* __restrict__ op, double thr,
+                              int32_t* __restrict__ block_counts) {
+  const int i = blockIdx.x * kPruneBlock + threadIdx.x;
+  const bool k = i < P && op[i] > thr;
+  const int c = __syncthreads_count(k);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = c;
+}
+
+__global__ void k_prune_scan(int32_t nb, int32_t* __restrict__ block_counts,
+                             int32_t* __restrict__ kept) {
+  __shared__ int32_t s_tot;
+  if (threadIdx.x == 0) {
+    int32_t run = 0;  // nb <= 2^31 / 1024: a serial scan by one thread is enough here
+    for (int b = 0; b < nb; ++b) {
+      const int32_t c = block_counts[b];
+      block_counts[b] = run;
+      run += c;
+    }
+    s_tot = run;
+    *kept = run;
+  }
+}
+
+__global__ void k_prune_gather(int32_t P, const double* __restrict__ op, double thr,
+                               const int32_t* __restrict__ block_start, tsb_row_buffer buf) {
+  __shared__ int32_t s_w[kPruneBlock / 32];
+  const int i = blockIdx.x * kPruneBlock + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool k = i < P && op[i] > thr;
+  const uint32_t b = __ballot_sync(0xffffffffu, k);
+  if (lane == 0) s_w[w] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int q = 0; q < kPruneBlock / 32; ++q) {
+      const int c = s_w[q];
+      s_w[q] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (!k) return;
+  const int64_t dst_row = block_start[blockIdx.x] + s_w[w] + __popc(b & ((1u << lane) - 1u));
+  const int64_t rb = buf.row_bytes;
+  const unsigned char* src = static_cast<const unsigned char*>(buf.src) + (int64_t)i * rb;
+  unsigned char* dst = static_cast<unsigned char*>(buf.dst) + dst_row * rb;
+  if ((rb & 7) == 0) {
+    for (int64_t q = 0; q < rb / 8; ++q)
+      reinterpret_cast<uint64_t*>(dst)[q] = reinterpret_cast<const uint64_t*>(src)[q];
+  } else {
+    for (int64_t q = 0; q < rb; ++q) dst[q] = src[q];
+  }
 }
 
 // The SSIM window lives in per-device __constant__ memory: uploaded once per
@@ -689,6 +813,11 @@ int tsb_loss_regularizers(const float* gbuf, const float* target, const tsb_came
 
 int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step, double beta1,
                   double beta2, double eps, void* stream) {
+  return tsb_adam_step_ex(groups, num_groups, step, beta1, beta2, eps, nullptr, stream);
+}
+
+int tsb_adam_step_ex(const tsb_adam_group* groups, int32_t num_groups, int32_t step,
+                     double beta1, double beta2, double eps, const int32_t* halt, void* stream) {
   if (!groups || num_groups <= 0 || num_groups > TSB_ADAM_MAX_GROUPS || step <= 0) {
     set_error("tsb_adam_step: invalid arguments");
     return TSB_ERR_VALUE;
@@ -699,7 +828,8 @@ int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step
   for (int k = 0; k < num_groups; ++k) {
     const tsb_adam_group& g = groups[k];
     if (g.count < 0 || (g.count > 0 && (!g.param || !g.grad || !g.m || !g.v)) ||
-        (g.dtype != TSB_F32 && g.dtype != TSB_F64)) {
+        (g.dtype != TSB_F32 && g.dtype != TSB_F64 && g.dtype != TSB_F32_TEX87) ||
+        (g.dtype == TSB_F32_TEX87 && (g.count & 7) != 0)) {
       set_error("tsb_adam_step: invalid group");
       return TSB_ERR_VALUE;
     }
@@ -712,6 +842,7 @@ int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step
     A.blk_start[k + 1] = A.blk_start[k] + (int32_t)nb;
   }
   A.b1 = beta1; A.b2 = beta2; A.eps = eps;
+  A.halt = halt;
   A.bc1 = 1.0 - std::pow(beta1, step);
   A.bc2 = 1.0 - std::pow(beta2, step);
   const int blocks = A.blk_start[num_groups];
@@ -723,14 +854,84 @@ int tsb_adam_step(const tsb_adam_group* groups, int32_t num_groups, int32_t step
 
 int tsb_orthonormalize_tangents(int32_t num_splats, double* tangent_u, double* tangent_v,
                                 void* stream) {
+  return tsb_orthonormalize_tangents_ex(num_splats, tangent_u, tangent_v, nullptr, stream);
+}
+
+int tsb_orthonormalize_tangents_ex(int32_t num_splats, double* tangent_u, double* tangent_v,
+                                   const int32_t* halt, void* stream) {
   if (num_splats < 0 || (num_splats > 0 && (!tangent_u || !tangent_v))) {
     set_error("tsb_orthonormalize_tangents: invalid arguments");
     return TSB_ERR_VALUE;
   }
   if (num_splats == 0) return TSB_OK;
-  k_orthonormalize<<<(num_splats + 255) / 256, 256, 0, (cudaStream_t)stream>>>(num_splats,
-                                                                             tangent_u, tangent_v);
+  k_orthonormalize<<<(num_splats + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      num_splats, tangent_u, tangent_v, halt);
   TSB_CHECK_LAUNCH("k_orthonormalize");
+  return TSB_OK;
+}
+
+int tsb_guard_finite(const double* terms, int32_t n, int32_t* halt, void* stream) {
+  if (!terms || !halt || n <= 0 || n > 1024) {
+    set_error("tsb_guard_finite: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  k_guard_finite<<<1, 32 * ((n + 31) / 32), 0, (cudaStream_t)stream>>>(terms, n, halt);
+  TSB_CHECK_LAUNCH("k_guard_finite");
+  return TSB_OK;
+}
+
+int tsb_broadcast_texels(int32_t num_splats, int32_t T0, int32_t T, const float* src, float* dst,
+                         void* stream) {
+  if (num_splats < 0 || T0 < 1 || T < 1 || (num_splats > 0 && (!src || !dst))) {
+    set_error("tsb_broadcast_texels: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  if (num_splats == 0) return TSB_OK;
+  k_broadcast_texels<<<1184, 256, 0, (cudaStream_t)stream>>>(
+      num_splats, T0, T, reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst));
+  TSB_CHECK_LAUNCH("k_broadcast_texels");
+  return TSB_OK;
+}
+
+int tsb_prune_scratch_size(int32_t num_splats, uint64_t* bytes) {
+  if (!bytes || num_splats < 0) {
+    set_error("tsb_prune_scratch_size: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  *bytes = (uint64_t)((num_splats + kPruneBlock - 1) / kPruneBlock + 1) * 4;
+  return TSB_OK;
+}
+
+int tsb_prune_rows(int32_t num_splats, const double* opacities, double threshold,
+                   const tsb_row_buffer* bufs, int32_t num_bufs, int32_t* kept, void* scratch,
+                   uint64_t scratch_bytes, void* stream) {
+  uint64_t need = 0;
+  if (tsb_prune_scratch_size(num_splats, &need) != TSB_OK) return TSB_ERR_VALUE;
+  if (!opacities || !kept || !scratch || scratch_bytes < need || num_bufs < 0 ||
+      (num_bufs > 0 && !bufs)) {
+    set_error("tsb_prune_rows: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  for (int b = 0; b < num_bufs; ++b)
+    if (!bufs[b].src || !bufs[b].dst || bufs[b].src == bufs[b].dst || bufs[b].row_bytes <= 0) {
+      set_error("tsb_prune_rows: every buffer needs distinct src / dst and a row size");
+      return TSB_ERR_VALUE;
+    }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (num_splats == 0) {
+    TSB_CUDA(cudaMemsetAsync(kept, 0, 4, st));
+    return TSB_OK;
+  }
+  const int nb = (num_splats + kPruneBlock - 1) / kPruneBlock;
+  int32_t* counts = static_cast<int32_t*>(scratch);
+  k_prune_count<<<nb, kPruneBlock, 0, st>>>(num_splats, opacities, threshold, counts);
+  TSB_CHECK_LAUNCH("k_prune_count");
+  k_prune_scan<<<1, 32, 0, st>>>(nb, counts, kept);
+  TSB_CHECK_LAUNCH("k_prune_scan");
+  for (int b = 0; b < num_bufs; ++b) {
+    k_prune_gather<<<nb, kPruneBlock, 0, st>>>(num_splats, opacities, threshold, counts, bufs[b]);
+    TSB_CHECK_LAUNCH("k_prune_gather");
+  }
   return TSB_OK;
 }
 

@@ -130,8 +130,8 @@ def test_orthonormalize_tangents_matches_reference():
 
 
 def test_trainer_step_gradient_equals_compute_step():
-    """The trainer's flat buffer (interleaved texel layout, fused packing)
-    holds exactly compute_step's gradients for the same parameters."""
+    """The trainer's flat buffer (7-channel combined texel gradients, fused
+    packing) holds exactly compute_step's gradients for the same parameters."""
     from paper_2506_13348_b200.training import DataParallelTrainer, compute_step
     truth = synth.make_gradcheck_scene(11)
     cam = synth.camera_ring(1, width=32, height=32)[0]
@@ -147,7 +147,93 @@ def test_trainer_step_gradient_equals_compute_step():
     assert abs(terms["loss"] - m["loss"]) <= 1e-6 * max(1.0, abs(m["loss"]))
     for name in ("positions", "tangent_u", "tangent_v", "scales", "opacities", "sh"):
         _close(name, getattr(tr.grads, name), getattr(grads, name), rel=1e-3)
-    got_tex = tr.grads.texels_dense[..., [0, 1, 2, 3, 6, 4, 5]]
-    _close("texels", got_tex, grads.texels_dense, rel=1e-3)
+    _close("texels", tr.grads.texels_dense, grads.texels_dense, rel=1e-3)
     for a, b in zip(tr.env_grads.spec_mips, eg.spec_mips):
         _close("env", a, b, rel=1e-3)
+
+
+def _train_golden():
+    from paper_2506_13348_b200.training import TrainConfig
+    g = gio.load("train_loop")
+    scene = gio.scene(g, "init_")
+    cams = [gio.camera(g, f"cam{i}_") for i in range(int(g["n_cams"]))]
+    targets = [g[f"target{i}"] for i in range(len(cams))]
+    cfg = TrainConfig(iterations=24, stage_split=12, texture_resolution=4, prune_interval=5,
+                      prune_opacity=0.005, seed=4)
+    return g, scene, cams, targets, cfg
+
+
+def test_train_loop_matches_reference_history():
+    """GPU train() vs the reference's train() (training.py:224-322) on the
+    same scene, views, targets and config: the same view schedule (numpy
+    default_rng(seed)), the stage-2 broadcast 1x1 -> 4x4 with the texel Adam
+    reset at iteration 12, the prune at iteration 5 (15 -> 12 splats, Adam
+    moments compacted), per-step losses within the fp32-vs-fp64 drift."""
+    from paper_2506_13348_b200.training import train
+    g, scene, cams, targets, cfg = _train_golden()
+    fitted, hist = train(scene, cams, targets, cfg, gio.lut())
+    assert [h["stage"] for h in hist] == list(g["h_stage"])
+    assert [h["splats"] for h in hist] == list(g["h_splats"])
+    frag = np.array([h["fragments"] for h in hist])
+    assert np.array_equal(frag[:5], g["h_fragments"][:5])  # before parameters drift
+    assert np.abs(frag - g["h_fragments"]).max() <= 1e-3 * g["h_fragments"].max()
+    ref = g["h_loss"]
+    got = np.array([h["loss"] for h in hist])
+    rel = np.abs(got - ref) / np.abs(ref)
+    print("train loop loss relative error per step:", rel.max(), rel)
+    # Stage 1 agrees to <= 8e-5 (observed over repeated runs). In stage 2
+    # (16 texels per splat, Adam reset) Adam's per-component normalisation
+    # turns the fp32 noise of near-zero texel gradients into full-size steps;
+    # on this 40x40, 12-splat problem one coverage decision can then flip a
+    # few steps later. Observed over repeated runs (scripts/train_drift.py):
+    # max 0.3 % or 7.7 % at one step depending on the run, run-to-run spread
+    # of the GPU itself of the same size.
+    stage2 = np.array([h["stage"] for h in hist]) == 2
+    assert rel[~stage2].max() <= 2e-4, rel
+    assert rel[stage2].max() <= 0.12, rel
+    assert np.median(rel[stage2]) <= 1e-2, rel
+    assert fitted.num_splats == 12 and fitted.texture_config.resolution == 4
+    assert fitted.texels.shape == (12, 4, 4, 7)
+
+
+def test_train_stage1_parameters_match_reference():
+    """Stage 1 only (12 iterations, prunes at 5 and 10): every fitted
+    parameter array, the texels and the environment vs the reference's."""
+    from paper_2506_13348_b200.training import train
+    g, scene, cams, targets, cfg = _train_golden()
+    cfg.iterations, cfg.stage_split = 12, 12
+    fitted, hist = train(scene, cams, targets, cfg, gio.lut())
+    assert [h["splats"] for h in hist] == list(g["s1_h_splats"])
+    rel = np.abs(np.array([h["loss"] for h in hist]) - g["s1_h_loss"]) / g["s1_h_loss"]
+    assert rel.max() <= 2e-4, rel
+    # Adam moves every component by ~lr per step whatever the gradient's size,
+    # so a near-zero fp32 gradient of the other sign costs (part of) a step:
+    # the bar is one step of each group's learning rate (observed: positions
+    # 1.7e-4 of 4.2e-4, env 5.2e-3 of 1e-2, opacities 3.2e-4 of 5e-2,
+    # texels 4.4e-5 of 2.5e-3)
+    errs = {}
+    for name in ("positions", "tangent_u", "tangent_v", "scales", "opacities", "sh"):
+        errs[name] = float(np.abs(getattr(fitted, name) - g[f"s1_fit_{name}"]).max())
+    errs["texels"] = float(np.abs(fitted.texels - g["s1_fit_texels"]).max())
+    errs["env"] = float(np.abs(fitted.environment.diffuse - g["s1_fit_env_diffuse"]).max())
+    print("stage-1 parameter errors:", errs)
+    from paper_2506_13348_b200.training import world_extent
+    step = {"positions": cfg.lr_position * world_extent(scene.positions),
+            "tangent_u": cfg.lr_frame, "tangent_v": cfg.lr_frame, "scales": cfg.lr_scale,
+            "opacities": cfg.lr_opacity, "sh": cfg.lr_sh, "texels": cfg.lr_texel,
+            "env": cfg.lr_env}
+    for name, e in errs.items():  # within one Adam step of the reference, per component
+        assert e <= step[name], (name, e, step[name])
+
+
+def test_train_loop_divergence_guard():
+    """A non-finite loss stops every later update on the device and raises
+    like the reference (training.py:263-265)."""
+    from paper_2506_13348_b200.training import train
+    g, scene, cams, targets, cfg = _train_golden()
+    bad = [t.copy() for t in targets]
+    for b in bad:
+        b[0, 0, 0] = np.nan
+    cfg.iterations = 6
+    with pytest.raises(RuntimeError, match="diverged"):
+        train(scene, cams, bad, cfg, gio.lut())
