@@ -5,15 +5,22 @@
 Workload (BASELINE.json configs[1], "cfg2"): make_shell_scene(100000, T=8,
 seed=3) with lobe_environment(default_rng(0), 64, 6), 800x800 views from the
 bench_cameras orbit (256 views, each rank takes views r, r+N, ...). One step =
-one frame: K1-K4 binning (preprocess, fp64 depth-rank sort, tile
-duplication + sort, ranges), K5 per-tile textured compositor (atlas fetched
-by the texture units), K6 deferred split-sum shading. Scene, atlas and
-environment are resident in HBM; L2 is flushed (256 MB write) between timed
-steps. Timed with CUDA events on the launch stream, max over ranks.
+one frame: binning (preprocess, 32-bit depth-key one-sweep sort with the
+fp64 run fix, duplication fused with the tile sort, ranges), K5 per-tile
+textured compositor (atlas fetched by the texture units), K6 deferred
+split-sum shading — one CUDA-graph replay per view. Scene, atlas and
+environment are resident in HBM. `value`: K frames back to back between a
+barrier + synchronize on both sides, CUDA events on the launch stream, max
+over ranks (inputs larger than L2: the 205 MB atlas alone exceeds the 126 MB
+L2). `breakdown_ms` / the roofline use a second pass with the L2 flushed
+(256 MB write) before every frame. --batch-views B (cfg3: 256): one step =
+the whole B-view orbit batch split over the ranks (strong scaling).
 
 --impl reference times the reference's CPU implementation of the same path:
-the C oracle port of texsplat's render_forward + shade_gbuffer (oracle/,
-the reference itself is numpy and does not travel), on all host threads.
+the C oracle port of texsplat's render_forward + shade_gbuffer (oracle/) on
+all host threads, K steps after W warm-up frames. The numpy reference
+itself (baseline/_ref) is timed inside the cpu_baseline leg on crop windows,
+single-process and one process per core (`cpu_baseline.numpy_reference`).
 """
 
 from __future__ import annotations
@@ -35,14 +42,16 @@ METRIC = "frames/sec at 800×800 (100k textured 2DGS) 1–8 B200; % TEX/HBM peak
 WORKLOAD = ("cfg2 (BASELINE configs[1]): 100k textured 2D Gaussians, 8x8 texel atlas, 800x800, "
             "forward + deferred envmap shading")
 CPU_BASELINE_NOTE = ("C oracle port of texsplat render_forward+shade_gbuffer (fp32, OpenMP over "
-                     "tiles); the numpy reference itself measured 0.0193 fps single-process on "
-                     "the survey host (SURVEY.md §6)")
+                     "tiles), the faster of the two CPU figures; the numpy reference itself is "
+                     "timed on the same host in numpy_reference (single process and one "
+                     "process per core)")
 
 
 # BASELINE.json configs; cfg2 is the headline workload.
 CONFIGS = {
     "cfg2": dict(splats=100_000, texture_res=8, width=800, height=800, env_height=64),
-    "cfg3": dict(splats=500_000, texture_res=8, width=1920, height=1080, env_height=64),
+    "cfg3": dict(splats=500_000, texture_res=8, width=1920, height=1080, env_height=64,
+                 batch_views=256),
     "cfg5": dict(splats=2_000_000, texture_res=16, width=1920, height=1080, env_height=128),
 }
 
@@ -67,6 +76,9 @@ def parse():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS),
                     help="BASELINE.json config preset (sets splats/texture/size/env)")
     ap.add_argument("--workload", default="render", choices=["render", "train"])
+    ap.add_argument("--batch-views", type=int, default=0,
+                    help="one step = a batch of this many orbit views over all ranks")
+    ap.add_argument("--no-numpy-reference", action="store_true")
     a = ap.parse_args()
     preset = CONFIGS[a.config]
     for k, v in preset.items():
@@ -166,13 +178,36 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    frames = max(1, args.steps)
-    for _ in range(min(args.warmup, 1)):
-        pass
-    fps, cores, sample, _ = cpu_baseline_run(args, min(frames, 5))
+    import numpy as np
+    from oracle import oracle
+    from paper_2506_13348_b200 import synth
+    from paper_2506_13348_b200.environment import BrdfLut
+
+    scene = synth.make_shell_scene(args.splats, args.texture_res, seed=3, with_environment=True,
+                                   env_height=args.env_height)
+    cams = synth.bench_cameras(256, args.width, args.height)
+    lut = BrdfLut.build()
+    atlas = oracle.pack(scene.texels)
+    cores = oracle.cpu_threads()
+    mode = "flat" if args.sampler == "flat" else "verify"
+
+    def frame(cam):
+        r = oracle.render(scene, cam, mode=mode, threads=cores, atlas=atlas)
+        oracle.shade(r["gbuf"], cam, scene.environment, lut.table, scene.background,
+                     threads=cores)
+
+    for i in range(args.warmup):
+        frame(cams[i % len(cams)])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        frame(cams[i % len(cams)])
+    dt = time.perf_counter() - t0
+    fps = args.steps / dt
+    sample = (f"{args.steps} full {args.width}x{args.height} frames (render_forward+"
+              f"shade_gbuffer), views 0..{args.steps - 1} after {args.warmup} warm-up frames")
     line = {
         "metric": METRIC, "value": round(fps, 6), "unit": "frames/s", "n_gpus": 0,
-        "steps": min(frames, 5), "warmup": 1, "ms_per_step": round(1e3 / fps, 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": WORKLOAD if args.config == "cfg2" else
@@ -189,7 +224,55 @@ def run_reference(args):
         "e2e": {"value": round(fps, 6), "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    del np
     print(json.dumps(line), flush=True)
+
+
+def numpy_reference_timing(args, frags_frame: float, procs: int):
+    """The numpy reference (baseline/_ref, texsplat itself) on crop windows
+    of view 0: single process (3 windows) and `procs` processes at once (2
+    windows each, one process per host core). A full frame is estimated per
+    window as prepare + render x F_frame / F_window + shade x pixels ratio
+    (crop windows are pixel-identical to the full frame)."""
+    if not (ROOT / "baseline" / "_ref" / "texsplat").exists():
+        return {"unavailable": "baseline/_ref/texsplat not installed"}
+    W, H = args.width, args.height
+    w = h = 96
+    xs = [int(W * f) - w // 2 for f in (0.35, 0.5, 0.65)]
+    ys = [int(H * f) - h // 2 for f in (0.35, 0.5, 0.65)]
+    windows = [(x, y, w, h) for y in ys for x in xs]
+
+    def launch(crops):
+        cmd = [sys.executable, str(ROOT / "scripts" / "numpy_ref_worker.py"), str(args.splats),
+               str(args.texture_res), str(W), str(H), str(args.env_height), "0"]
+        cmd += [",".join(str(v) for v in c) for c in crops]
+        return subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                text=True, env=dict(os.environ, OMP_NUM_THREADS="1",
+                                                    OPENBLAS_NUM_THREADS="1"))
+
+    def frame_s(rec):
+        f = max(rec["fragments"], 1)
+        return (rec["prepare_s"] + rec["render_s"] * frags_frame / f
+                + rec["shade_s"] * (W * H) / (rec["crop"][2] * rec["crop"][3]))
+
+    try:
+        p = launch(windows[3:6])
+        single = json.loads(p.communicate(timeout=600)[0].strip().splitlines()[-1])
+        t_single = statistics.median(frame_s(r) for r in single)
+        ps = [launch([windows[(2 * i) % 9], windows[(2 * i + 1) % 9]]) for i in range(procs)]
+        par = []
+        for q in ps:
+            par += json.loads(q.communicate(timeout=900)[0].strip().splitlines()[-1])
+        t_par = statistics.median(frame_s(r) for r in par)
+    except Exception as e:  # noqa: BLE001 — report, do not fail the bench
+        return {"unavailable": f"numpy reference run failed: {e!r}"[:200]}
+    return {"fps_single_process": round(1.0 / t_single, 5),
+            "fps_process_parallel": round(procs / t_par, 5), "cores": procs,
+            "frame_s_single": round(t_single, 3), "frame_s_parallel_each": round(t_par, 3),
+            "sample": f"texsplat (numpy, baseline/_ref) atlas-mode prepare + render_forward + "
+                      f"shade_gbuffer of 96x96 windows of view 0, extrapolated to the "
+                      f"{W}x{H} frame by fragment count ({frags_frame:.0f}); 3 windows single-"
+                      f"process, {procs} processes x 2 windows at once"}
 
 
 def run_train(args, scene, cams, lut, rank, world, dev):
@@ -284,7 +367,10 @@ def main():
     r = Renderer(scene, atlas, scene.environment, lut, texture_mode=texture_mode,
                  sampler=None if args.sampler == "flat" else args.sampler,
                  texel_format=args.texel_format, tile=args.tile)
-    my_views = [cams[i] for i in range(rank, len(cams), world)]
+    if args.batch_views > 0:  # one step = the first batch_views orbit views over all ranks
+        my_views = [cams[i] for i in range(rank, min(args.batch_views, len(cams)), world)]
+    else:
+        my_views = [cams[i] for i in range(rank, len(cams), world)]
 
     # size the workspace from every view of this rank once (no per-frame host
     # sync later); the device-side running maximum of the entry counts
@@ -348,29 +434,43 @@ def main():
     shade_ms = [e[2].elapsed_time(e[3]) for e in events]
     phased_ms = [e[0].elapsed_time(e[3]) for e in events]
 
-    # timed steps: the whole frame (K1-K6) replayed as one CUDA graph per view
+    # timed steps: K steps back to back, one CUDA-graph replay per frame,
+    # between a barrier + synchronize on both sides (inputs larger than L2)
     graph, _ = r._graph(my_views[0], W, H)
     cams_c = [_lib.camera_struct(c) for c in my_views]
-    gevents = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
-    for i in range(args.warmup):
+    batch = args.batch_views > 0
+    per_step = len(cams_c) if batch else 1
+
+    def launch(i):
         _lib.check(L.tsb_frame_graph_launch(graph, C.byref(cams_c[i % len(cams_c)]),
                                             _lib.ptr(col), sh), "graph")
+
+    for i in range(args.warmup * per_step):
+        launch(i)
+    # diagnostic: the same frames with the L2 flushed before each one
+    KF = min(K, 30)
+    gevents = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(KF)]
+    for i in range(KF):
+        flush.zero_()
+        gevents[i][0].record(stream)
+        launch(i)
+        gevents[i][1].record(stream)
+    torch.cuda.synchronize()
+    frame_ms = [e[0].elapsed_time(e[1]) for e in gevents]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(gpu)
     clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    for i in range(K):
-        flush.zero_()  # L2 flush (outside the timed events)
-        gevents[i][0].record(stream)
-        _lib.check(L.tsb_frame_graph_launch(graph, C.byref(cams_c[i % len(cams_c)]),
-                                            _lib.ptr(col), sh), "graph")
-        gevents[i][1].record(stream)
+    ev0.record(stream)
+    for i in range(K * per_step):
+        launch(i)
+    ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    frame_ms = [e[0].elapsed_time(e[1]) for e in gevents]
-    total_ms = sum(frame_ms)
+    total_ms = ev0.elapsed_time(ev1)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -382,7 +482,8 @@ def main():
     # Renderer.stream_views: each frame's colour image lands in pinned host
     # memory; frame i's device->host copy overlaps frame i+1's render.
     cam_bytes = C.sizeof(_lib.Camera_t)
-    e2e_views = [my_views[i % len(my_views)] for i in range(args.e2e_steps)]
+    e2e_views = (list(my_views) if batch else
+                 [my_views[i % len(my_views)] for i in range(args.e2e_steps)])
     for _ in r.stream_views(e2e_views[:4]):
         pass
     torch.cuda.synchronize()
@@ -395,7 +496,7 @@ def main():
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_fps = world * args.e2e_steps / float(te.item())
+    e2e_fps = (args.batch_views if batch else world * args.e2e_steps) / float(te.item())
 
     # ---- TEX peak probe (same texture, L1-resident window) ------------------
     tex_peak = None
@@ -459,24 +560,59 @@ def main():
     hbm_achieved = alg_bytes / rast_avg_s / 1e9
     fetch_rate = 2 * fragments / rast_avg_s / 1e9 if args.sampler != "flat" else 0.0
 
-    value = world * K / (max_ms * 1e-3)
+    value = (K * args.batch_views if batch else world * K) / (max_ms * 1e-3)
+    verify_fps = None
+    if args.sampler == "hw" and world == 1 and not batch:
+        # like-for-like with the CPU arms (fp32 software bilinear = verify mode)
+        rv = Renderer(scene, atlas, scene.environment, lut, texture_mode="atlas",
+                      sampler="verify", tile=args.tile)
+        rv.reserve(my_views[0], ws.capacity)
+        for i in range(3):
+            rv.render(my_views[i], check=False)
+        gv, _ = rv._graph(my_views[0], W, H)
+        gcol = rv._buffers(W, H)[2]
+        torch.cuda.synchronize()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        for i in range(K):
+            _lib.check(L.tsb_frame_graph_launch(gv, C.byref(cams_c[i % len(cams_c)]),
+                                                _lib.ptr(gcol), sh), "graph")
+        v1.record(stream)
+        torch.cuda.synchronize()
+        verify_fps = K / (v0.elapsed_time(v1) * 1e-3)
+        rv.check_capacity()
+        rv.close()
+        del rv
+    view0_frags = None
+    if world == 1 and not args.no_cpu_baseline:  # fragments of view 0 (numpy extrapolation)
+        r.render(cams[0], check=True)
+        view0_frags = float(px.n_contrib.sum(dtype=torch.int64).item())
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(max_ms / K, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if batch else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD if args.config == "cfg2" else
                    f"{args.config}: {P} textured 2D Gaussians, {T}x{T} atlas, {W}x{H}",
                    "splats": P, "texture_res": T, "width": W,
                    "height": H, "sampler": args.sampler, "texel_format": args.texel_format,
-                   "tile": args.tile, "views": "bench_cameras(256) orbit, rank r takes r::N",
-                   "l2": "flushed between timed steps (256 MB write, outside the events)",
+                   "tile": args.tile,
+                   "views": (f"one step = the {args.batch_views}-view bench_cameras orbit batch, "
+                             f"rank r renders views r::N" if batch else
+                             "bench_cameras(256) orbit, rank r takes r::N, one view per step"),
+                   "l2": "inputs larger than L2 (fp32 atlas 205 MB at cfg2 > 126 MB L2): "
+                         "frames back to back, no flush; breakdown_ms.frame_median_l2_flushed "
+                         "repeats frames with a 256 MB L2 flush before each",
                    "parallelism": f"views partitioned over {world} GPU(s), scene replicated"},
         "breakdown_ms": {"binning": round(statistics.mean(bin_ms), 4),
                          "raster": round(statistics.mean(rast_ms), 4),
                          "shade": round(statistics.mean(shade_ms), 4),
-                         "frame_median": round(statistics.median(frame_ms), 4),
+                         "frame_median_l2_flushed": round(statistics.median(frame_ms), 4),
                          "frame_median_launches": round(statistics.median(phased_ms), 4)},
+        "verify_sampler_fps": None if verify_fps is None else round(verify_fps, 3),
+        "verify_sampler_note": "the same frames with the fp32 software-bilinear sampler "
+                               "(verify mode), the arithmetic the CPU reference arm runs: "
+                               "the like-for-like ratio is verify_sampler_fps / reference",
         "fragments_per_frame": fragments, "entries_per_frame": entries,
         "capacity_overflow": bool(overflow),
         "roofline": {"bound": "hbm", "kernel": "k_raster_fwd", "achieved": round(hbm_achieved, 2),
@@ -503,17 +639,23 @@ def main():
                         "binning, so it runs under frame i+1's rasteriser; camera passed by "
                         "value in the launch; scene, atlas, environment resident (uploaded "
                         "once)"},
-        "gpu_launches": 7 * K,
-        "gpu_launches_note": "ours per frame (one CUDA graph replay per view): k_preprocess, "
-                             "k_fix_runs_rank, k_duplicate_lb, k_ranges, k_tile_schedule, "
-                             "k_raster_fwd, k_shade; the same graph also holds 11 CUB kernels "
-                             "(depth and tile radix sorts, the tile-count scan) launched by "
-                             "libtsb.so",
+        "gpu_launches": 13 * K * per_step,
+        "gpu_launches_note": "ours per frame (one CUDA graph replay per view, no library "
+                             "kernels): k_preprocess, 4 x k_onesweep (depth), k_fix_runs, "
+                             "k_sort_long_runs, k_dup_tx, k_onesweep (tile rows), k_ranges, "
+                             "k_tile_schedule, k_raster_fwd, k_shade (+ 2 memset nodes)",
     }
     if world == 1 and not args.no_cpu_baseline:
         fps, cores, sample, _ = cpu_baseline_run(args, args.cpu_frames)
         line["cpu_baseline"] = {"value": round(fps, 6), "unit": "frames/s", "cores": cores,
                                 "kind": "port", "sample": sample, "note": CPU_BASELINE_NOTE}
+        if not args.no_numpy_reference and view0_frags:
+            npr = numpy_reference_timing(args, view0_frags, cores)
+            line["cpu_baseline"]["numpy_reference"] = npr
+            if "fps_single_process" in npr:
+                line["vs_numpy_reference"] = {
+                    "e2e_over_single_process": round(e2e_fps / npr["fps_single_process"], 1),
+                    "e2e_over_process_parallel": round(e2e_fps / npr["fps_process_parallel"], 1)}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
