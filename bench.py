@@ -277,11 +277,16 @@ def numpy_reference_timing(args, frags_frame: float, procs: int):
 
 def run_train(args, scene, cams, lut, rank, world, dev):
     """cfg4: data-parallel training steps (forward + shade + loss + backward +
-    NCCL all-reduce + Adam), each rank on its own views."""
+    bucketed all-reduce + Adam), each rank on its own views."""
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
 
-    from paper_2506_13348_b200 import render_forward, shade_gbuffer
+    from paper_2506_13348_b200 import _lib, render_forward, shade_gbuffer
+    from paper_2506_13348_b200.backward import splat_backward
+    from paper_2506_13348_b200.rasterize import render_prepared
+    from paper_2506_13348_b200.shading import shade_planar
     from paper_2506_13348_b200.training import (DataParallelTrainer, linear_to_display,
                                                 partition_views)
     views = [cams[i] for i in partition_views(len(cams), rank, world)]
@@ -297,33 +302,165 @@ def run_train(args, scene, cams, lut, rank, world, dev):
     for i in range(args.warmup):
         tr.step(views[i % nt], targets[i % nt])
     torch.cuda.synchronize()
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
         terms, _ = tr.step(views[i % nt], targets[i % nt])
     e1.record()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # ---- e2e: the public step with host data every step --------------------
+    # target image copied from pinned host memory, loss read back, per step
+    host_tgts = [tg.cpu().pin_memory() for tg in targets]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    loss_sum = 0.0
+    for i in range(args.steps):
+        tgt = host_tgts[i % nt].to(dev, non_blocking=True)
+        terms_i, _ = tr.step(views[i % nt], tgt)
+        loss_sum += terms_i["loss"]  # D2H of the step's loss terms
+    e2e_s = time.perf_counter() - t0
+    clk = clocks.stop()
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = world * args.steps / float(te.item())
+
+    # ---- roofline of the dominant kernel: K8 (k_raster_bwd) ---------------
+    # K8 alone on view 0 (events around splat_backward), the global atomic
+    # adds it issues (device counter), and the RED throughput peak measured
+    # live with tsb_red_probe (scattered float adds, L2-resident buffer)
+    L = _lib.lib()
+    cam0, tgt0 = views[0], targets[0]
+    H, W = int(cam0.height), int(cam0.width)
+    tr.grads_and_loss(cam0, tgt0)
+    gbuf, tape = render_prepared(tr.prep, cam0, tr.tile, check=True)
+    dg = torch.randn((13, H, W), dtype=torch.float32, device=dev) * 1e-3
+    for _ in range(2):
+        splat_backward(None, cam0, tr.prep, tape, dg, grads=tr.grads, scratch=tr.bwd_scratch)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kr = 5
+    torch.cuda.synchronize()
+    k0.record()
+    for _ in range(kr):
+        splat_backward(None, cam0, tr.prep, tape, dg, grads=tr.grads, scratch=tr.bwd_scratch)
+    k1.record()
+    torch.cuda.synchronize()
+    k8_ms = k0.elapsed_time(k1) / kr
+    cnt = C.c_ulonglong()
+    _lib.check(L.tsb_debug_red_count(1, None), "red count")
+    splat_backward(None, cam0, tr.prep, tape, dg, grads=tr.grads, scratch=tr.bwd_scratch)
+    torch.cuda.synchronize()
+    _lib.check(L.tsb_debug_red_count(0, C.byref(cnt)), "red count")
+    reds = int(cnt.value)
+    fragments = int(gbuf.pixels.n_contrib.sum(dtype=torch.int64).item())
+    pbuf = torch.zeros(1 << 23, dtype=torch.float32, device=dev)  # 32 MB, L2-resident
+    blocks, threads, iters = 148 * 16, 256, 256
+    for _ in range(2):
+        L.tsb_red_probe(_lib.ptr(pbuf), 23, iters, blocks, threads, _lib.stream_handle())
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for _ in range(5):
+        L.tsb_red_probe(_lib.ptr(pbuf), 23, iters, blocks, threads, _lib.stream_handle())
+    p1.record()
+    torch.cuda.synchronize()
+    red_peak = 5 * blocks * threads * iters / (p0.elapsed_time(p1) * 1e-3) / 1e9  # G adds/s
+    red_rate = reds / (k8_ms * 1e-3) / 1e9
+
     if rank == 0:
-        ms = float(t.item())
-        print(json.dumps({
+        line = {
             "metric": "training steps/s (cfg4: 100k textured 2DGS, 800x800, DP over views)",
             "value": round(world * args.steps / (ms * 1e-3), 3), "unit": "view-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "cfg4 training step", "splats": args.splats,
-                       "texture_res": args.texture_res, "width": args.width,
-                       "height": args.height, "allreduce": "one NCCL all-reduce of the flat "
-                       "fp32 gradient buffer per step"},
-            "last_loss": terms["loss"]}), flush=True)
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg4 training step (BASELINE configs[3]): forward + shade + "
+                       "loss + backward into atlas and Gaussian params + all-reduce + Adam",
+                       "splats": args.splats, "texture_res": args.texture_res,
+                       "width": args.width, "height": args.height,
+                       "allreduce": "bucketed async all-reduce of the flat fp32 gradient buffer "
+                                    "(geometry + env, then 4 texel buckets of 7-channel "
+                                    "gradients), Adam per bucket",
+                       "parallelism": f"data parallel over views, {world} GPU(s)"},
+            "last_loss": terms["loss"],
+            "roofline": {"bound": "l2_atomics", "kernel": "k_raster_bwd",
+                         "achieved": round(red_rate, 3), "peak": round(red_peak, 3),
+                         "unit": "G float atomic adds/s", "frac": round(red_rate / red_peak, 4),
+                         "traffic": None, "k8_ms": round(k8_ms, 4),
+                         "atomic_adds_per_launch": reds, "fragments": fragments,
+                         "algorithmic_adds_before_warp_reduction": 28 * fragments,
+                         "peak_source": "measured live: tsb_red_probe, scattered float adds "
+                                        "into a 32 MB L2-resident buffer",
+                         "note": "adds issued counted on the device (tsb_debug_red_count); K8 "
+                                 "reduces each live splat's 22 terms and each bilinear cell's "
+                                 "28 texel values over the warp before one add"},
+            "clocks": clk,
+            "e2e": {"value": round(e2e, 3), "unit": "view-steps/s",
+                    "h2d_bytes_per_step": H * W * 3 * 4, "d2h_bytes_per_step": 8 * 8,
+                    "note": "DataParallelTrainer.step with the view's display target copied "
+                            "from pinned host memory and the step's loss terms read back "
+                            "every step"},
+            "gpu_launches": None,
+        }
+        if world == 1 and not args.no_cpu_baseline and not args.no_numpy_reference:
+            line["cpu_baseline"] = numpy_train_timing(args, fragments)
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def numpy_train_timing(args, frags_frame: float):
+    """The reference's compute_step (numpy, baseline/_ref) on 64x64 windows
+    of view 0, extrapolated to the full frame by fragment count: one process
+    (2 windows) and one process per core (1 window each)."""
+    from oracle import oracle
+    if not (ROOT / "baseline" / "_ref" / "texsplat").exists():
+        return {"unavailable": "baseline/_ref/texsplat not installed"}
+    W, H = args.width, args.height
+    procs = oracle.cpu_threads()
+    windows = [(int(W * fx) - 32, int(H * fy) - 32, 64, 64)
+               for fy in (0.4, 0.5, 0.6) for fx in (0.4, 0.5, 0.6)]
+
+    def launch(crops):
+        cmd = [sys.executable, str(ROOT / "scripts" / "numpy_ref_worker.py"), "--train",
+               str(args.splats), str(args.texture_res), str(W), str(H), str(args.env_height),
+               "0"] + [",".join(str(v) for v in c) for c in crops]
+        return subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                text=True, env=dict(os.environ, OMP_NUM_THREADS="1",
+                                                    OPENBLAS_NUM_THREADS="1"))
+
+    def step_s(r):
+        return r["prepare_s"] + (r["step_s"] - r["prepare_s"]) * frags_frame / max(r["fragments"], 1)
+
+    try:
+        one = json.loads(launch(windows[3:5]).communicate(timeout=900)[0].strip().splitlines()[-1])
+        t1 = statistics.median(step_s(r) for r in one)
+        ps = [launch([windows[i % 9]]) for i in range(procs)]
+        par = []
+        for q in ps:
+            par += json.loads(q.communicate(timeout=900)[0].strip().splitlines()[-1])
+        tp = statistics.median(step_s(r) for r in par)
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"numpy reference run failed: {e!r}"[:200]}
+    return {"value": round(1.0 / t1, 6), "unit": "view-steps/s", "cores": 1, "kind": "reference",
+            "process_parallel": {"value": round(procs / tp, 6), "cores": procs},
+            "sample": f"texsplat compute_step (numpy, baseline/_ref) on 64x64 windows of view 0 "
+                      f"(2 single-process, {procs} concurrent processes x 1), extrapolated to "
+                      f"the {W}x{H} frame by fragment count ({frags_frame:.0f})"}
 
 
 def main():

@@ -207,6 +207,13 @@ int tsb_atlas_tex_create(const float* family_a, const float* family_b, int32_t p
                          tsb_atlas_tex_t* out, void* stream);
 int tsb_atlas_tex_destroy(tsb_atlas_tex_t tex);
 
+/* Measurement: `blocks` x `threads` threads each issue `iters` float atomic
+ * adds to pseudo-random addresses of a 2^log2_floats-float buffer (the
+ * gradient scatter of K8 without contention): the RED throughput peak the
+ * training roofline divides by. */
+int tsb_red_probe(float* buf, int32_t log2_floats, int32_t iters, int32_t blocks, int32_t threads,
+                  void* stream);
+
 /* TEX-unit throughput probe used by bench.py for the TEX roofline: `fetches`
  * bilinear RGBA fetches spread over an L1-resident window of the atlas.
  * Writes a checksum per thread into sink (grid*block floats). */
@@ -285,6 +292,11 @@ int tsb_render_backward_ex(const tsb_scene* scene, const tsb_camera* camera,
                            const tsb_pixel_state* pixels, const float* dgbuf, void* scratch,
                            tsb_scene_grads* grads, int32_t deterministic, void* det_scratch,
                            uint64_t det_scratch_bytes, void* stream);
+
+/* Diagnostics (synchronous): reads the number of global atomic adds the
+ * backward rasterizer issued since the last call into *count (may be NULL),
+ * resets it, and switches counting on (enable != 0) or off. */
+int tsb_debug_red_count(int32_t enable, unsigned long long* count);
 
 /* Scratch bytes of the deterministic backward for P splats at T x T texels
  * in `texel_layout` (TSB_TEXELS_COMBINED / TSB_TEXELS_INTERLEAVED). */

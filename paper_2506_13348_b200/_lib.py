@@ -112,6 +112,8 @@ _SIGNATURES = {
                              C.POINTER(C.c_void_p), _P],
     "tsb_atlas_tex_destroy": [_P],
     "tsb_tex_probe": [_P, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P],
+    "tsb_red_probe": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P],
+    "tsb_debug_red_count": [C.c_int32, C.POINTER(C.c_ulonglong)],
     "tsb_shade_backward": [_P, C.POINTER(Camera_t), C.POINTER(Environment_t), _P, _P, _P,
                            C.POINTER(EnvGrads_t), _P, C.c_uint64, _P],
     "tsb_shade_backward_scratch_size": [C.POINTER(Environment_t), C.POINTER(C.c_uint64)],

@@ -40,6 +40,20 @@ constexpr int kAccWords = 24;  // per-splat accumulator stride (22 used)
 // rounded to the grid once; the sums are then exact, so bitwise repeatable.
 constexpr int kAccFix = 32, kTexFix = 40;
 
+// Diagnostics (tsb_debug_red_count): with a counter in the launch parameters,
+// K8 counts the global atomic adds it issues (one warp-aggregated add per
+// warp and site), for the training roofline's achieved RED rate.
+__device__ unsigned long long g_red_count = 0ull;
+static bool g_count_red_host = false;
+
+__device__ __forceinline__ void count_red(unsigned long long* ctr, bool issued) {
+  if (ctr) {
+    const uint32_t b = __ballot_sync(__activemask(), issued);
+    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && b)
+      atomicAdd(ctr, (unsigned long long)__popc(b));
+  }
+}
+
 __device__ __forceinline__ unsigned long long to_fix(float v, int shift) {
   return (unsigned long long)__double2ll_rn((double)v * (double)(1ull << shift));
 }
@@ -358,6 +372,7 @@ struct RasterBwdParams {
   // atomics above (integer adds commute, so any order gives the same bits)
   unsigned long long* acc64;  // P x kAccWords, value * 2^kAccFix
   unsigned long long* tex64;  // P x T x T x tl, value * 2^kTexFix
+  unsigned long long* red_count;  // diagnostics: atomic adds issued (or null)
   int32_t tl;          // channels per texel: 7 (combined) or 8 (interleaved)
   int32_t num_tiles;
   int32_t* work_counter;
@@ -650,6 +665,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
           const int nl = __popc(lm);
           float tot = 0.f;
           for (int i = 0; i < nl; ++i) tot += ws.red[28 * i + lane];
+          count_red(p.red_count, tot != 0.0f);
           if (tot != 0.0f) {
             if constexpr (DET)
               atomicAdd(p.acc64 + (size_t)kAccWords * id + lane, to_fix(tot, kAccFix));
@@ -683,6 +699,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
               for (uint32_t m = grp; m; m &= m - 1) tsum += ws.red[36 * (__ffs(m) - 1) + lane];
               const int* lr = reinterpret_cast<const int*>(ws.red + 36 * l + 28);
               const int off = lr[0] + ((t_corner & 1) ? lr[1] : 0) + ((t_corner & 2) ? lr[2] : 0) + t_slot;
+              count_red(p.red_count, tsum != 0.0f);
               if (tsum != 0.0f) {
                 if constexpr (DET)
                   atomicAdd(p.tex64 + (size_t)id * T * T * tl + off, to_fix(tsum, kTexFix));
@@ -876,6 +893,15 @@ int tsb_backward_scratch_size(int32_t P, uint64_t* bytes) {
   return TSB_OK;
 }
 
+int tsb_debug_red_count(int32_t enable, unsigned long long* count) {
+  g_count_red_host = enable != 0;
+  TSB_CUDA(cudaDeviceSynchronize());
+  if (count) TSB_CUDA(cudaMemcpyFromSymbol(count, g_red_count, sizeof(unsigned long long)));
+  const unsigned long long z = 0ull;
+  TSB_CUDA(cudaMemcpyToSymbol(g_red_count, &z, sizeof(z)));
+  return TSB_OK;
+}
+
 int tsb_backward_det_scratch_size(int32_t P, int32_t T, int32_t texel_layout, uint64_t* bytes) {
   if (!bytes || P < 0 || T < 1 ||
       (texel_layout != TSB_TEXELS_COMBINED && texel_layout != TSB_TEXELS_INTERLEAVED)) {
@@ -1032,6 +1058,8 @@ int tsb_render_backward_ex(const tsb_scene* scene, const tsb_camera* camera,
   rp.tl = grads->texel_layout == TSB_TEXELS_INTERLEAVED ? 8 : 7;
   const int64_t n_acc = (int64_t)P * kAccWords;
   const int64_t n_tex = (int64_t)P * atlas->resolution * atlas->resolution * rp.tl;
+  rp.red_count = nullptr;
+  if (g_count_red_host) TSB_CUDA(cudaGetSymbolAddress((void**)&rp.red_count, g_red_count));
   rp.acc64 = deterministic ? static_cast<unsigned long long*>(det_scratch) : nullptr;
   rp.tex64 = deterministic ? rp.acc64 + n_acc : nullptr;
   if (deterministic)

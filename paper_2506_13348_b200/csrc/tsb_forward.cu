@@ -778,6 +778,17 @@ __global__ void k_tex_probe(cudaTextureObject_t tex, int32_t window, int32_t ite
   sink[t] = acc;
 }
 
+// Scattered float atomic adds into an L2-resident buffer (the backward's
+// gradient scatter pattern, no contention): the RED throughput peak for the
+// K8 roofline. Each thread issues `iters` independent adds.
+__global__ void k_red_probe(float* __restrict__ buf, uint32_t mask, int32_t iters) {
+  uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u;
+  for (int k = 0; k < iters; ++k) {
+    h = h * 1664525u + 1013904223u;
+    atomicAdd(buf + ((h >> 7) & mask), 1.0f);
+  }
+}
+
 template <int TILE, int MODE>
 inline cudaError_t launch_raster_mode(int blocks, cudaStream_t st, const RasterParams& rp) {
   constexpr int threads = 32 * TSB_RASTER_WARPS;
@@ -1220,6 +1231,17 @@ int tsb_debug_stats(unsigned long long* out, int reset) {
   return 0;
 }
 #endif
+
+int tsb_red_probe(float* buf, int32_t log2_floats, int32_t iters, int32_t blocks, int32_t threads,
+                  void* stream) {
+  if (!buf || log2_floats < 1 || log2_floats > 30 || iters <= 0 || blocks <= 0 || threads <= 0) {
+    set_error("tsb_red_probe: invalid arguments");
+    return TSB_ERR_VALUE;
+  }
+  k_red_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(buf, (1u << log2_floats) - 1u, iters);
+  TSB_CHECK_LAUNCH("k_red_probe");
+  return TSB_OK;
+}
 
 int tsb_tex_probe(tsb_atlas_tex_t h, int32_t window, int32_t iters, float* sink, int32_t blocks,
                   int32_t threads, void* stream) {

@@ -566,26 +566,31 @@ __device__ __forceinline__ void adam_chunk_f4(const AdamLaunch& A, const tsb_ada
 // slot 7 stays untouched.
 __device__ __forceinline__ void adam_chunk_tex87(const AdamLaunch& A, const tsb_adam_group& g,
                                                  int64_t base) {
-  float* prm = static_cast<float*>(g.param);
-  float* m = static_cast<float*>(g.m);
-  float* v = static_cast<float*>(g.v);
+  // one texel (8 parameter slots, 7 gradients) per thread: 128-bit parameter
+  // and moment accesses (the group's arrays are 32-B aligned per texel)
+  float4* prm = static_cast<float4*>(g.param);
+  float4* m4 = static_cast<float4*>(g.m);
+  float4* v4 = static_cast<float4*>(g.v);
   const float b1 = (float)A.b1, b2 = (float)A.b2, c1 = (float)(1.0 - A.b1), c2 = (float)(1.0 - A.b2);
   const float ibc1 = (float)(1.0 / A.bc1), ibc2 = (float)(1.0 / A.bc2), lr = (float)g.lr;
   const float eps = (float)A.eps;
-  constexpr int kSlotToCombined[8] = {0, 1, 2, 3, 5, 6, 4, -1};
-#pragma unroll 4
-  for (int j = 0; j < kAdamChunk / 256; ++j) {
-    const int64_t i = base + j * 256 + threadIdx.x;
-    if (i >= g.count) break;
-    const int slot = (int)(i & 7);
-    const int c = kSlotToCombined[slot];
-    if (c < 0) continue;
-    const float gr = __ldg(g.grad + (i >> 3) * 7 + c);
-    float mi = m[i], vi = v[i];
-    prm[i] = adam_f(prm[i], gr, mi, vi, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
-    m[i] = mi;
-    v[i] = vi;
-  }
+  const int64_t q = base / 8 + threadIdx.x;  // texel
+  if (q >= g.count / 8) return;
+  const float* gr = g.grad + q * 7;  // combined: alb rgb, rough, metal, nrm a, nrm b
+  float4 p0 = prm[2 * q], p1 = prm[2 * q + 1];
+  float4 ma = m4[2 * q], mb = m4[2 * q + 1];
+  float4 va = v4[2 * q], vb = v4[2 * q + 1];
+  // slots: p0 = (alb r, g, b, rough), p1 = (nrm a, nrm b, metal, pad)
+  p0.x = adam_f(p0.x, __ldg(gr + 0), ma.x, va.x, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+  p0.y = adam_f(p0.y, __ldg(gr + 1), ma.y, va.y, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+  p0.z = adam_f(p0.z, __ldg(gr + 2), ma.z, va.z, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+  p0.w = adam_f(p0.w, __ldg(gr + 3), ma.w, va.w, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+  p1.x = adam_f(p1.x, __ldg(gr + 5), mb.x, vb.x, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+  p1.y = adam_f(p1.y, __ldg(gr + 6), mb.y, vb.y, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+  p1.z = adam_f(p1.z, __ldg(gr + 4), mb.z, vb.z, b1, b2, c1, c2, ibc1, ibc2, lr, eps, g);
+  prm[2 * q] = p0; prm[2 * q + 1] = p1;
+  m4[2 * q] = ma; m4[2 * q + 1] = mb;
+  v4[2 * q] = va; v4[2 * q + 1] = vb;
 }
 
 __global__ void __launch_bounds__(256) k_adam(AdamLaunch A) {

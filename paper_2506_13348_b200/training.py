@@ -337,7 +337,12 @@ class DataParallelTrainer:
                                   workspace=self.workspace)
         n_geom = sum(t.numel() for t in p.values())
         n_env = sum(t.numel() for t in self.env_params)
-        n_tex = P * T * T * 7
+        # texel gradients: 7 combined channels when they go on the wire (no
+        # zero pad channel in the all-reduce); on one GPU the 8-channel
+        # interleaved layout of the parameters themselves (32-B aligned texels:
+        # fewer L2 sectors per atomic in K8, vectorised Adam)
+        self.tex_ch = 7 if _dist_on() else 8
+        n_tex = P * T * T * self.tex_ch
         self.n_geom, self.n_env, self.n_tex = n_geom, n_env, n_tex
         self.flat = torch.zeros(n_geom + n_env + n_tex, dtype=torch.float32, device=dev)
         self.geom64 = torch.zeros(n_geom, dtype=torch.float64, device=dev)
@@ -345,10 +350,11 @@ class DataParallelTrainer:
         for n in _GEOM:
             gviews[n] = self.geom64[o:o + p[n].numel()].view(p[n].shape)
             o += p[n].numel()
-        tex_grad = self.flat[n_geom + n_env:].view(P, T, T, 7)
+        tex_grad = self.flat[n_geom + n_env:].view(P, T, T, self.tex_ch)
         self.grads = SceneGrads(gviews["positions"], gviews["tangent_u"], gviews["tangent_v"],
                                 gviews["scales"], gviews["opacities"], gviews["sh"], tex_grad,
-                                texel_layout=_lib.TEXELS_COMBINED)
+                                texel_layout=(_lib.TEXELS_COMBINED if self.tex_ch == 7
+                                              else _lib.TEXELS_INTERLEAVED))
         env_views, o = [], n_geom
         for prm in self.env_params:
             env_views.append(self.flat[o:o + prm.numel()].view(prm.shape))
@@ -390,9 +396,11 @@ class DataParallelTrainer:
             if b <= a:
                 continue
             tex_groups.append((f"texels:{i}", self.texels8[a:b], tex_grad[a:b],
-                               self.lr["texels"], _lib.CLAMP_UNIT, _lib.F32_TEX87,
+                               self.lr["texels"], _lib.CLAMP_UNIT,
+                               _lib.F32_TEX87 if self.tex_ch == 7 else _lib.F32,
                                tm[a:b], tv[a:b]))
-            tex_ranges.append((n_geom + n_env + a * T * T * 7, n_geom + n_env + b * T * T * 7))
+            c = self.tex_ch
+            tex_ranges.append((n_geom + n_env + a * T * T * c, n_geom + n_env + b * T * T * c))
         self._buckets = [((0, n_geom + n_env), first)] + [
             (rng, [g]) for rng, g in zip(tex_ranges, tex_groups)]
         self._launches = []
@@ -486,23 +494,39 @@ class DataParallelTrainer:
             stepped.update(names)
         for n in stepped:
             self.steps[n] = self.steps.get(n, 0) + 1
-        works = self._allreduce_async()
-        for (rng, arr, n, names), work in zip(self._launches, works):
-            if n == 0:
-                continue
-            if work is not None:
+        if _dist_on():
+            works = self._allreduce_async()
+            for (rng, arr, n, names), work in zip(self._launches, works):
+                if n == 0:
+                    continue
                 work.wait()  # (the current stream waits on this bucket only)
-            if self.group is not None or _dist_on():
                 self.flat[rng[0]:rng[1]].div_(_world(self.group))
-            t = self.steps[names[0]]
-            _lib.check(L.tsb_adam_step_ex(arr, n, t, float(self.betas[0]), float(self.betas[1]),
-                                          float(self.eps), _lib.ptr(self.halt), sh),
-                       "tsb_adam_step")
+                t = self.steps[names[0]]
+                _lib.check(L.tsb_adam_step_ex(arr, n, t, float(self.betas[0]),
+                                              float(self.betas[1]), float(self.eps),
+                                              _lib.ptr(self.halt), sh), "tsb_adam_step")
+        else:  # one GPU: one Adam launch per distinct step count (normally one)
+            for t, (arr, n) in self._single_launches().items():
+                _lib.check(L.tsb_adam_step_ex(arr, n, t, float(self.betas[0]),
+                                              float(self.betas[1]), float(self.eps),
+                                              _lib.ptr(self.halt), sh), "tsb_adam_step")
         if self.optimize_geometry:
             _lib.check(L.tsb_orthonormalize_tangents_ex(
                 self.P, _lib.ptr(self.params["tangent_u"]), _lib.ptr(self.params["tangent_v"]),
                 _lib.ptr(self.halt), sh), "tsb_orthonormalize_tangents")
         return st, self.flat
+
+    def _single_launches(self):
+        """Every bucket's groups merged, keyed by their Adam step count."""
+        by_t = {}
+        for _, arr, n, names in self._launches:
+            for i in range(n):
+                by_t.setdefault(self.steps[names[i]], []).append(arr[i])
+        out = {}
+        for t, gs in by_t.items():
+            arr = (_lib.AdamGroup_t * len(gs))(*gs)
+            out[t] = (arr, len(gs))
+        return out
 
     def _allreduce_async(self):
         """Start one all-reduce (sum) per bucket; None entries: no group."""
