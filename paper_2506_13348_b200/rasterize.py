@@ -73,7 +73,17 @@ class PixelState:
 class GBuffer:
     """Blended attribute buffers; all channels coverage-premultiplied."""
 
-    def __init__(self, planar: torch.Tensor, pixels: PixelState = None):
+    def __init__(self, planar, pixels: PixelState = None):
+        """`planar`: a (13, H, W) float32 device tensor, or — like the
+        reference's GBuffer(data) (rasterize.py:62-67) — an (H, W, 13) array
+        (numpy or tensor), uploaded to the current device as planar float32."""
+        if not (torch.is_tensor(planar) and planar.is_cuda and planar.dim() == 3
+                and planar.shape[0] == NUM_CHANNELS and planar.dtype == torch.float32):
+            t = planar if torch.is_tensor(planar) else torch.from_numpy(
+                np.ascontiguousarray(np.asarray(planar), dtype=np.float32))
+            if t.dim() != 3 or t.shape[-1] != NUM_CHANNELS:
+                raise ValueError(f"G-buffer data must be (H, W, {NUM_CHANNELS})")
+            planar = t.to(device="cuda", dtype=torch.float32).permute(2, 0, 1).contiguous()
         self.planar = planar          # (13, H, W) float32
         self.pixels = pixels
 
