@@ -483,6 +483,10 @@ def main():
     # (TSB_BENCH_DEVICE / TSB_BENCH_BACKEND: test hooks that run every rank on
     # one GPU over gloo to exercise the multi-rank code path on a 1-GPU box)
     gpu = int(os.environ.get("TSB_BENCH_DEVICE", local))
+    shared_device = world > 1 and "TSB_BENCH_DEVICE" in os.environ
+    if shared_device and os.environ.get("TSB_BENCH_BACKEND", "nccl") == "nccl":
+        raise SystemExit("TSB_BENCH_DEVICE puts every rank on one GPU: set "
+                         "TSB_BENCH_BACKEND=gloo (NCCL cannot share a device)")
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
     if world > 1:
@@ -635,6 +639,27 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_fps = (args.batch_views if batch else world * args.e2e_steps) / float(te.item())
 
+    # ---- e2e through texsplat's own per-view loop (cli.py:63-68) ----------
+    # render_forward(scene, cam, "atlas", atlas) + shade_gbuffer(...) per view
+    # with the reference's objects, colour to a numpy array each view: the
+    # one-shot API (device copies cached per host object, resident.py)
+    loop_fps = None
+    if world == 1 and not batch and args.sampler == "hw":
+        from paper_2506_13348_b200 import render_forward, shade_gbuffer
+        nl = min(args.e2e_steps, 50)
+        for cam in my_views[:3]:
+            gbl = render_forward(scene, cam, "atlas", atlas, texel_format=args.texel_format)
+            shade_gbuffer(gbl, cam, scene.environment, lut, background=scene.background)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(nl):
+            cam = my_views[i % len(my_views)]
+            gbl = render_forward(scene, cam, "atlas", atlas, texel_format=args.texel_format)
+            srl = shade_gbuffer(gbl, cam, scene.environment, lut, background=scene.background)
+            img = srl.color.cpu().numpy()
+        loop_fps = nl / (time.perf_counter() - t0)
+        del img
+
     # ---- TEX peak probe (same texture, L1-resident window) ------------------
     tex_peak = None
     if prep.atlas.tex is not None:
@@ -776,6 +801,14 @@ def main():
                         "binning, so it runs under frame i+1's rasteriser; camera passed by "
                         "value in the launch; scene, atlas, environment resident (uploaded "
                         "once)"},
+        "e2e_reference_loop": None if loop_fps is None else {
+            "value": round(loop_fps, 3), "unit": "frames/s",
+            "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": H * W * 3 * 4,
+            "note": "texsplat's cmd_render per-view body (cli.py:63-68) through the drop-in "
+                    "API: render_forward + shade_gbuffer with the same host scene / atlas / "
+                    "environment objects, colour copied to numpy every view, synchronously "
+                    "(no overlap of the copy with the next view, a host sync per view for "
+                    "the capacity check)"},
         "gpu_launches": 13 * K * per_step,
         "gpu_launches_note": "ours per frame (one CUDA graph replay per view, no library "
                              "kernels): k_preprocess, 4 x k_onesweep (depth), k_fix_runs, "
@@ -793,6 +826,10 @@ def main():
                 line["vs_numpy_reference"] = {
                     "e2e_over_single_process": round(e2e_fps / npr["fps_single_process"], 1),
                     "e2e_over_process_parallel": round(e2e_fps / npr["fps_process_parallel"], 1)}
+    if shared_device:  # every rank on one GPU: a code-path check, not a measurement
+        line["shared_device"] = True
+        line["value"] = None
+        line["e2e"]["value"] = None
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
