@@ -380,6 +380,10 @@ def run_train(args, scene, cams, lut, rank, world, dev):
     torch.cuda.synchronize()
     red_peak = 5 * blocks * threads * iters / (p0.elapsed_time(p1) * 1e-3) / 1e9  # G adds/s
     red_rate = reds / (k8_ms * 1e-3) / 1e9
+    k8_traffic = None
+    tjp = ROOT / "profiles" / "traffic.json"
+    if tjp.exists():
+        k8_traffic = json.loads(tjp.read_text()).get("cfg4/k_raster_bwd")
 
     if rank == 0:
         line = {
@@ -400,7 +404,9 @@ def run_train(args, scene, cams, lut, rank, world, dev):
             "roofline": {"bound": "l2_atomics", "kernel": "k_raster_bwd",
                          "achieved": round(red_rate, 3), "peak": round(red_peak, 3),
                          "unit": "G float atomic adds/s", "frac": round(red_rate / red_peak, 4),
-                         "traffic": None, "k8_ms": round(k8_ms, 4),
+                         "traffic": k8_traffic, "k8_ms": round(k8_ms, 4),
+                         "traffic_source": "profiles/traffic.json (ncu --set full DRAM bytes "
+                                           "read + written by one k_raster_bwd launch)",
                          "atomic_adds_per_launch": reds, "fragments": fragments,
                          "algorithmic_adds_before_warp_reduction": 28 * fragments,
                          "peak_source": "measured live: tsb_red_probe, scattered float adds "

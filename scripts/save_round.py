@@ -27,29 +27,44 @@ for f in sorted(src.glob("*.json")):
         shutil.copy(f, dst / f"{tag}_{f.stem}.json")
 if table3:
     (dst / f"{tag}_table3.json").write_text(json.dumps(table3, indent=1) + "\n")
-shutil.copy(src / "launches.csv", dst / f"{tag}_launches.csv")
-if (src / "train_launches.csv").exists():
-    shutil.copy(src / "train_launches.csv", dst / f"{tag}_train_launches.csv")
-subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_summary.py"), str(src / "launches.csv"),
-                str(src / "full.ncu-rep"), str(dst / f"{tag}_ncu_summary.md")], check=True,
-               stdout=subprocess.DEVNULL)
+for name in ("launches", "launches_cfg5", "train_launches"):
+    if (src / f"{name}.csv").exists():
+        shutil.copy(src / f"{name}.csv", dst / f"{tag}_{name}.csv")
+summ = [("launches", "full", "ncu_summary"), ("launches_cfg5", "full_cfg5", "ncu_summary_cfg5"),
+        ("train_launches", "full_bwd", "ncu_summary_train")]
+for lname, rname, oname in summ:
+    if (src / f"{lname}.csv").exists() and (src / f"{rname}.ncu-rep").exists():
+        subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_summary.py"),
+                        str(src / f"{lname}.csv"), str(src / f"{rname}.ncu-rep"),
+                        str(dst / f"{tag}_{oname}.md")], check=True, stdout=subprocess.DEVNULL)
 M = ("dram__bytes_read.sum,dram__bytes_write.sum,l1tex__throughput.avg.pct_of_peak_sustained_active,"
      "dram__cycles_active.avg.pct_of_peak_sustained_elapsed,"
-     "l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed")
-raw = subprocess.run(["ncu", "-i", str(src / "full.ncu-rep"), "--page", "raw", "--csv", "--metrics", M],
-                     capture_output=True, text=True).stdout
-rows = list(csv.DictReader(io.StringIO(raw)))
-for r in rows[1:]:
-    if "k_raster_fwd" in r["Kernel Name"]:
-        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        unit_r, unit_w = rows[0]["dram__bytes_read.sum"], rows[0]["dram__bytes_write.sum"]
-        tb = (float(r["dram__bytes_read.sum"]) * mult[unit_r] +
-              float(r["dram__bytes_write.sum"]) * mult[unit_w])
-        out = {"cfg2/hw/rgba32f": int(tb),
-               "ncu": {"kernel": "k_raster_fwd (cfg2, hw, rgba32f)",
-                       "l1tex_throughput_pct": float(r["l1tex__throughput.avg.pct_of_peak_sustained_active"]),
-                       "tex_data_pipe_pct": float(r["l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed"]),
-                       "dram_throughput_pct": float(r["dram__cycles_active.avg.pct_of_peak_sustained_elapsed"])}}
-        (dst / "traffic.json").write_text(json.dumps(out) + "\n")
-        print("k_raster_fwd", out)
+     "l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed,gpu__time_duration.sum")
+mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+traffic = {}
+for rname, key in (("full", "cfg2/hw/rgba32f"), ("full_cfg5", "cfg5/hw/rgba32f"),
+                   ("full_bwd", "cfg4/k_raster_bwd")):
+    rep = src / f"{rname}.ncu-rep"
+    if not rep.exists():
+        continue
+    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv", "--metrics", M],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.DictReader(io.StringIO(raw)))
+    for r in rows[1:]:
+        want = "k_raster_bwd" if "bwd" in rname else "k_raster_fwd"
+        if want not in r["Kernel Name"]:
+            continue
+        tb = (float(r["dram__bytes_read.sum"]) * mult[rows[0]["dram__bytes_read.sum"]] +
+              float(r["dram__bytes_write.sum"]) * mult[rows[0]["dram__bytes_write.sum"]])
+        traffic[key] = int(tb)
+        traffic[key.replace("/", "_") + "_ncu"] = {
+            "kernel": f"{want} ({key})",
+            "duration_us": float(r["gpu__time_duration.sum"]),
+            "l1tex_throughput_pct": float(r["l1tex__throughput.avg.pct_of_peak_sustained_active"]),
+            "tex_data_pipe_pct": float(r["l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed"]),
+            "dram_throughput_pct": float(r["dram__cycles_active.avg.pct_of_peak_sustained_elapsed"])}
         break
+if "cfg2/hw/rgba32f" in traffic:
+    traffic["ncu"] = traffic["cfg2_hw_rgba32f_ncu"]
+(dst / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+print(json.dumps(traffic, indent=1))
