@@ -79,6 +79,9 @@ def parse():
     ap.add_argument("--batch-views", type=int, default=0,
                     help="one step = a batch of this many orbit views over all ranks")
     ap.add_argument("--no-numpy-reference", action="store_true")
+    ap.add_argument("--pipeline", type=int, default=3,
+                    help="views in flight: independent workspaces on separate streams "
+                         "(1 = one view at a time)")
     a = ap.parse_args()
     preset = CONFIGS[a.config]
     for k, v in preset.items():
@@ -587,10 +590,14 @@ def main():
     cams_c = [_lib.camera_struct(c) for c in my_views]
     batch = args.batch_views > 0
     per_step = len(cams_c) if batch else 1
+    npipe = max(1, args.pipeline)
+    pipes = [(graph, col, stream)] + [
+        (*r._graph(my_views[0], W, H, slot=j), torch.cuda.Stream(dev)) for j in range(1, npipe)]
 
     def launch(i):
-        _lib.check(L.tsb_frame_graph_launch(graph, C.byref(cams_c[i % len(cams_c)]),
-                                            _lib.ptr(col), sh), "graph")
+        g_, c_, s_ = pipes[i % npipe]
+        _lib.check(L.tsb_frame_graph_launch(g_, C.byref(cams_c[i % len(cams_c)]),
+                                            _lib.ptr(c_), _lib.stream_handle(s_)), "graph")
 
     for i in range(args.warmup * per_step):
         launch(i)
@@ -600,7 +607,7 @@ def main():
     for i in range(KF):
         flush.zero_()
         gevents[i][0].record(stream)
-        launch(i)
+        launch(i * npipe)  # (slot 0, the timing stream)
         gevents[i][1].record(stream)
     torch.cuda.synchronize()
     frame_ms = [e[0].elapsed_time(e[1]) for e in gevents]
@@ -611,8 +618,14 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
+    for _, _, s_ in pipes[1:]:
+        s_.wait_event(ev0)
     for i in range(K * per_step):
         launch(i)
+    for _, _, s_ in pipes[1:]:  # join the other frame streams
+        ej = torch.cuda.Event()
+        ej.record(s_)
+        stream.wait_event(ej)
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -631,12 +644,12 @@ def main():
     cam_bytes = C.sizeof(_lib.Camera_t)
     e2e_views = (list(my_views) if batch else
                  [my_views[i % len(my_views)] for i in range(args.e2e_steps)])
-    for _ in r.stream_views(e2e_views[:4]):
+    for _ in r.stream_views(e2e_views[:4], pipeline=npipe):
         pass
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     checksum = 0.0
-    for _, host_img in r.stream_views(e2e_views):
+    for _, host_img in r.stream_views(e2e_views, pipeline=npipe):
         checksum += float(host_img[H // 2, W // 2, 0])
     e2e_s = time.perf_counter() - t0
     clk = clocks.stop()
@@ -771,7 +784,8 @@ def main():
                    "l2": "inputs larger than L2 (fp32 atlas 205 MB at cfg2 > 126 MB L2): "
                          "frames back to back, no flush; breakdown_ms.frame_median_l2_flushed "
                          "repeats frames with a 256 MB L2 flush before each",
-                   "parallelism": f"views partitioned over {world} GPU(s), scene replicated"},
+                   "parallelism": f"views partitioned over {world} GPU(s), scene replicated",
+                   "frames_in_flight": npipe},
         "breakdown_ms": {"binning": round(statistics.mean(bin_ms), 4),
                          "raster": round(statistics.mean(rast_ms), 4),
                          "shade": round(statistics.mean(shade_ms), 4),
@@ -802,11 +816,11 @@ def main():
         "e2e": {"value": round(e2e_fps, 3), "unit": "frames/s",
                 "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": H * W * 3 * 4,
                 "note": "Renderer.stream_views: render + D2H of every frame's (H,W,3) float32 "
-                        "colour into pinned host memory, host consumes each image; frame i's "
-                        "copy starts from an event recorded inside frame i+1's graph after its "
-                        "binning, so it runs under frame i+1's rasteriser; camera passed by "
-                        "value in the launch; scene, atlas, environment resident (uploaded "
-                        "once)"},
+                        "colour into pinned host memory, host consumes each image in order; "
+                        "frames_in_flight views in independent workspaces on their own "
+                        "streams, each colour copied out on a copy stream as its view "
+                        "completes; camera passed by value in the launch; scene, atlas, "
+                        "environment resident (uploaded once)"},
         "e2e_reference_loop": None if loop_fps is None else {
             "value": round(loop_fps, 3), "unit": "frames/s",
             "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": H * W * 3 * 4,

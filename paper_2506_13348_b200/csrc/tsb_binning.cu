@@ -173,13 +173,14 @@ __global__ void __launch_bounds__(kOsThreads) k_onesweep(OnesweepArgs a) {
   const int K = a.kept ? *a.kept : n;
   const int nr = a.mode == kOsLater ? K : n;
   if (tid == 0) s_bid = atomicAdd(a.ticket, 1);
+  __syncthreads();
+  const int bid = s_bid;
+  if (bid * TILE >= n) return;  // (CTAs beyond the items: before any scan)
   for (int i = tid; i < kOsWarps * (int)(kRadixBins + 1); i += kOsThreads) (&whist[0][0])[i] = 0u;
   digit_offsets(a.hist, a.hist_is_diff, s_goff, s_warp);  // (syncs the block)
   // a later depth pass whose digit is the same for every kept item is the identity
   const bool trivial =
       a.mode == kOsLater && __syncthreads_or(a.hist[tid] == K && K > 0);
-  const int bid = s_bid;
-  if (bid * TILE >= n) return;
   uint32_t key[ITEMS], val[ITEMS];
   const int base = bid * TILE + w * (TILE / kOsWarps);
 #pragma unroll
@@ -282,11 +283,12 @@ __global__ void __launch_bounds__(kOsThreads) k_dup_tx(DupArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t E = *a.total;
   if (tid == 0) s_bid = atomicAdd(a.ticket, 1);
-  for (int i = tid; i < kOsWarps * (int)(kRadixBins + 1); i += kOsThreads) (&whist[0][0])[i] = 0u;
-  digit_offsets(a.hist_tx, true, s_goff, s_warp);
+  __syncthreads();
   const int bid = s_bid;
   const int K = *a.kept;
-  if (E > a.cap || bid * kOsThreads >= K) return;
+  if (E > a.cap || bid * kOsThreads >= K) return;  // (before any scan)
+  for (int i = tid; i < kOsWarps * (int)(kRadixBins + 1); i += kOsThreads) (&whist[0][0])[i] = 0u;
+  digit_offsets(a.hist_tx, true, s_goff, s_warp);
   const int r = bid * kOsThreads + tid;
   uint32_t cnt = 0, box = 0;
   int32_t sl = 0;
@@ -510,15 +512,18 @@ template __global__ void k_onesweep<16>(OnesweepArgs a);
 __global__ void k_ranges(int64_t cap, const uint32_t* __restrict__ keys,
                          const int64_t* __restrict__ counters, int32_t* __restrict__ ranges,
                          int64_t* __restrict__ max_needed) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = counters[0];
-  if (i == 0)  // running max over frames (tsb_frame_workspace_max_needed_offset)
+  if (blockIdx.x == 0 && threadIdx.x == 0)  // running max (tsb_frame_workspace_max_needed_offset)
     atomicMax(reinterpret_cast<unsigned long long*>(max_needed), (unsigned long long)total);
   if (total > cap) total = 0;  // overflowed frame: leave every tile empty
-  if (i >= total) return;
-  const uint32_t t = keys[i];
-  if (i == 0 || keys[i - 1] != t) ranges[2 * t] = (int32_t)i;
-  if (i == total - 1 || keys[i + 1] != t) ranges[2 * t + 1] = (int32_t)(i + 1);
+  // grid-stride over the frame's entries (a fixed grid: the capacity does not
+  // cost launch work)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = keys[i];
+    if (i == 0 || keys[i - 1] != t) ranges[2 * t] = (int32_t)i;
+    if (i == total - 1 || keys[i + 1] != t) ranges[2 * t + 1] = (int32_t)(i + 1);
+  }
 }
 
 }  // namespace tsb

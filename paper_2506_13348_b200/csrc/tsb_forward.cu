@@ -157,14 +157,21 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   // SH coefficients read in place (a local copy would live in local memory)
   const double* sh = p.sh + (size_t)3 * K * id;
   tsb_prep r;
-  tsb_preprocess_splat(&p.cam, pos, tu, tv, s, sh, p.sh_degree, &r);
+  tsb_prep_cull(&p.cam, pos, tu, tv, s, &r);  // centre depth, rect, keep
+  p.rects[id] = make_uint2((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
+                           (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
+  p.ids[id] = id;
+  if (!r.keep) {  // culled: no M / frame / SH work, no entries, sorts last
+    p.tile_count[id] = 0;
+    p.dkeys[id] = ~0ull;
+    p.dkey32[id] = kDepthCulled32;
+  } else {
+  tsb_prep_kept(&p.cam, pos, tu, tv, s, sh, p.sh_degree, &r);
   const double op = p.op[id];
 
   GeomRec g;
   tsb_make_lin(r.m, op, g.lin);
   g.r2lo = tsb_lin_r2lo(g.lin[11]);
-  p.rects[id] = make_uint2((uint32_t)r.x0 | ((uint32_t)r.x1 << 16),
-                           (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
   int32_t tb[4];
   tsb_test_box(&p.cam, r.m, g.lin[11], r.x0, r.x1, r.y0, r.y1, tb);
   g.bx = (uint32_t)tb[0] | ((uint32_t)tb[1] << 16);
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   // Tile binning by the test box (reference rect ∩ alpha-cut ellipse box):
   // a strictly tighter, conservative version of _tile_lists' rect binning
   // (rasterize.py:246-258) — tiles outside it cannot hold a live pixel.
-  const bool binned = r.keep && tb[1] > tb[0] && tb[3] > tb[2];
+  const bool binned = tb[1] > tb[0] && tb[3] > tb[2];
   int32_t ntiles = 0;
   if (binned) {
     const int tx0 = tb[0] / p.tile, tx1 = (tb[1] - 1) / p.tile;
@@ -192,12 +199,11 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   // patterns; 2^-20 relative resolution, no clamping); k_fix_runs re-orders
   // equal keys by the full 64-bit pattern => the exact (z, id) order.
   const uint64_t full = tsb_f64_bits(r.view_z);
-  p.dkeys[id] = r.keep ? full : ~0ull;
-  const uint32_t k32 = r.keep ? (uint32_t)(full >> 32) - p.near_hi : kDepthCulled32;
+  p.dkeys[id] = full;
+  const uint32_t k32 = (uint32_t)(full >> 32) - p.near_hi;
   p.dkey32[id] = k32;
-  p.ids[id] = id;
   kkey = k32;  // (the depth histograms count kept splats only)
-  kkept = r.keep ? 1 : 0;
+  kkept = 1;
   ktiles = (uint32_t)ntiles;
   // the rasterizer and the backward read records only through tile-list
   // entries: splats without entries (culled, or no pixel in the box) skip them
@@ -224,6 +230,7 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   for (int k = 0; k < 9; ++k) m64[k] = r.m[k];
   m64[9] = op;
   }
+  }  // kept
   }
   // warp-aggregated histogram updates (equal digits of a warp: one atomic)
   {
@@ -1011,7 +1018,8 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     k_onesweep<kOsItems><<<L.nb_tiley, kOsThreads, 0, st>>>(ya);
     TSB_CHECK_LAUNCH("k_onesweep(tile_y)");
     const int64_t C = std::max<int64_t>(cap, 1);
-    k_ranges<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(cap, ya.kout, counters, ranges,
+    k_ranges<<<(unsigned)std::min<int64_t>((C + 255) / 256, 148 * 16), 256, 0, st>>>(
+        cap, ya.kout, counters, ranges,
                                                           ws_ptr<int64_t>(ws, L.max_needed));
     TSB_CHECK_LAUNCH("k_ranges");
   }

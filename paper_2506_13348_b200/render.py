@@ -92,20 +92,43 @@ class Renderer:
             raise RuntimeError(f"frame workspace overflow: a frame needed {need} tile entries, "
                                f"capacity {ws.capacity}; reserve() more and re-render")
 
-    def _graph(self, camera, W, H, binned_event=None):
+    def _slot(self, W, H, slot):
+        """(workspace, buffers) of frame slot `slot`: slot 0 is the prepared
+        scene's own workspace; further slots (pipelined views, see
+        stream_views) get their own workspace of the same capacity."""
+        if slot == 0:
+            return self.prep.workspace, self._buffers(W, H)
+        key = ("slot", W, H, slot)
+        ws0 = self.prep.workspace
+        if key not in self._bufs:
+            self._bufs[key] = (FrameWorkspace(self.device), None)
+        ws = self._bufs[key][0]
+        if ws0.key is not None and (ws.key != ws0.key or ws.capacity != ws0.capacity):
+            ws.ensure(*ws0.key, ws0.capacity, exact=True)
+        bkey = ("slotbuf", W, H, slot)
+        if bkey not in self._bufs:
+            dev = self.device
+            self._bufs[bkey] = (
+                torch.empty((NUM_CHANNELS, H, W), dtype=torch.float32, device=dev),
+                PixelState.empty(H, W, dev),
+                torch.empty((H, W, 3), dtype=torch.float32, device=dev), None, None)
+        return ws, self._bufs[bkey]
+
+    def _graph(self, camera, W, H, binned_event=None, slot: int = 0):
         """CUDA graph of this view size over the current buffers (rebuilt if
         the workspace was reallocated). `binned_event`: a torch.cuda.Event the
-        graph records between binning and rasterisation on every replay."""
-        ws = self.prep.workspace
-        gb, px, col, _, _ = self._buffers(W, H)
+        graph records between binning and rasterisation on every replay.
+        `slot`: an independent workspace + buffer set (pipelined views)."""
+        ws, bufs = self._slot(W, H, slot)
+        gb, px, col = bufs[0], bufs[1], bufs[2]
         ev = None if binned_event is None else binned_event.cuda_event
         key = (_lib.ptr(ws.buf), ws.capacity, ws.nbytes, ev)
-        cur = self._graphs.get((W, H, ev))
+        cur = self._graphs.get((W, H, ev, slot))
         if cur is not None and cur[0] == key:
             return cur[1], col
         if cur is not None:
             _lib.lib().tsb_frame_graph_destroy(cur[1])
-            del self._graphs[(W, H, ev)]
+            del self._graphs[(W, H, ev, slot)]
         L = _lib.lib()
         sc, at, cam = self.prep.scene.struct(), self.prep.atlas.struct(), _lib.camera_struct(camera)
         pst = px.struct()
@@ -119,7 +142,7 @@ class Renderer:
             _lib.ptr(ws.buf), ws.nbytes, ws.capacity, _lib.ptr(gb), C.byref(pst),
             _lib.ptr(ws.needed), C.byref(env), bg, _lib.ptr(col), None, None,
             C.c_void_p(ev) if ev else None, C.byref(h)), "tsb_frame_graph_create_ev")
-        self._graphs[(W, H, ev)] = (key, h)
+        self._graphs[(W, H, ev, slot)] = (key, h)
         return h, col
 
     def close(self):
@@ -166,14 +189,88 @@ class Renderer:
                      want_split=want_split, stream=stream)
         return col, gbuf
 
-    def stream_views(self, cameras, host_out=None, depth: int = 2):
+    def _stream_pipelined(self, cams, host_out, depth, n):
+        """stream_views with `n` frames in flight: frame i renders in slot
+        i % n (its own workspace and buffers) on that slot's stream, so the
+        latency-bound binning of one view overlaps the rasteriser tail of the
+        previous; colour goes to a ring of `depth` device buffers (no frame
+        waits for an earlier frame's copy unless the ring wraps) and is copied
+        out on a copy stream once its frame is done. Yields (i, host image)
+        in order, or (i, None) at the first frame whose slot reported a
+        tile-entry overflow (the caller grows and resumes)."""
+        W, H = int(cams[0].width), int(cams[0].height)
+        dev = self.device
+        depth = max(n + 2, int(depth))
+        key = ("pipe", W, H, n, depth)
+        if key not in self._bufs:
+            self._bufs[key] = (
+                [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(depth)],
+                [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True)
+                 for _ in range(depth)],
+                [torch.cuda.Stream(dev) for _ in range(n)], torch.cuda.Stream(dev),
+                torch.zeros((depth,), dtype=torch.int64, pin_memory=True))
+        dcol, hcol_cached, streams, copy, hmax = self._bufs[key]
+        hcol = host_out or hcol_cached
+        graphs = [self._graph(cams[0], W, H, slot=j)[0] for j in range(n)]
+        wss = [self._slot(W, H, j)[0] for j in range(n)]
+        cur = torch.cuda.current_stream(dev)
+        start = torch.cuda.Event()
+        for ws in wss:
+            ws.reset_max()
+        start.record(cur)
+        for st in streams:
+            st.wait_event(start)
+        cdone = [None] * len(cams)
+
+        def emit(i):
+            b = i % depth
+            cdone[i].synchronize()
+            return i, (hcol[b] if int(hmax[b]) <= wss[i % n].capacity else None)
+
+        lag = depth - 1  # frames in flight beyond the one being consumed
+        for i, cam in enumerate(cams):
+            j, b = i % n, i % depth
+            st = streams[j]
+            if i >= depth:  # ring buffer b: the copy of frame i - depth is done
+                st.wait_event(cdone[i - depth])
+            cs = _lib.camera_struct(cam)
+            _lib.check(_lib.lib().tsb_frame_graph_launch(graphs[j], C.byref(cs),
+                                                         _lib.ptr(dcol[b]),
+                                                         _lib.stream_handle(st)),
+                       "tsb_frame_graph_launch")
+            fdone = torch.cuda.Event()
+            fdone.record(st)
+            copy.wait_event(fdone)
+            with torch.cuda.stream(copy):
+                hcol[b].copy_(dcol[b], non_blocking=True)
+                hmax[b:b + 1].copy_(wss[j].max_needed, non_blocking=True)
+            cdone[i] = torch.cuda.Event()
+            cdone[i].record(copy)
+            if i >= lag:  # host buffer b is rewritten `depth` frames later
+                k, img = emit(i - lag)
+                yield k, img
+                if img is None:
+                    return
+        for k in range(max(0, len(cams) - lag), len(cams)):
+            kk, img = emit(k)
+            yield kk, img
+            if img is None:
+                return
+        for st in streams:
+            end = torch.cuda.Event()
+            end.record(st)
+            cur.wait_event(end)
+
+    def stream_views(self, cameras, host_out=None, depth: int = 2, pipeline: int = 3):
         """Render a sequence of views and read each colour image back to
         pinned host memory (`depth` rotating output buffers, a dedicated copy
         stream). Frame i's device->host copy starts once frame i+1's tile
         lists are built (an event recorded inside the frame graph), so it
         overlaps frame i+1's rasteriser rather than its latency-bound
         binning. Yields (index, host colour tensor) in order as each copy
-        completes; a host buffer is reused `depth` frames later.
+        completes; a host buffer is reused `depth` frames later. pipeline > 1:
+        that many frames in flight in independent workspaces on their own
+        streams (_stream_pipelined).
 
         Capacity: with every image the device's running maximum of the
         frames' entry counts comes back too. A frame is yielded only once it
@@ -183,16 +280,22 @@ class Renderer:
         start = 0
         while start < len(cams):
             resume = None
-            for i, img in self._stream(cams[start:], host_out, depth):
+            W, H = int(cams[0].width), int(cams[0].height)
+            gen = (self._stream_pipelined(cams[start:], host_out, depth, pipeline)
+                   if pipeline > 1 and self._graph_ready(W, H)
+                   else self._stream(cams[start:], host_out, depth))
+            for i, img in gen:
                 if img is None:       # overflow detected: frames >= i unverified
                     resume = start + i
                     break
                 yield start + i, img
             if resume is None:
                 return
-            torch.cuda.current_stream(self.device).synchronize()
+            torch.cuda.synchronize(self.device)
             ws = self.prep.workspace
-            need = ws.max_needed_value()
+            need = max([ws.max_needed_value()] + [
+                v[0].max_needed_value() for k, v in self._bufs.items()
+                if isinstance(k, tuple) and k[0] == "slot"])
             c = cams[resume]
             ws.ensure(self.prep.scene.num_splats, int(c.width), int(c.height), self.tile,
                       int(need * 1.25) + 4096)

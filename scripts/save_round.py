@@ -59,7 +59,8 @@ for rname, key in (("full", "cfg2/hw/rgba32f"), ("full_cfg5", "cfg5/hw/rgba32f")
         traffic[key] = int(tb)
         traffic[key.replace("/", "_") + "_ncu"] = {
             "kernel": f"{want} ({key})",
-            "duration_us": float(r["gpu__time_duration.sum"]),
+            "duration_us": float(r["gpu__time_duration.sum"]) * {
+                "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}[rows[0]["gpu__time_duration.sum"]],
             "l1tex_throughput_pct": float(r["l1tex__throughput.avg.pct_of_peak_sustained_active"]),
             "tex_data_pipe_pct": float(r["l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed"]),
             "dram_throughput_pct": float(r["dram__cycles_active.avg.pct_of_peak_sustained_elapsed"])}

@@ -88,7 +88,7 @@ def test_stream_views_recovers_from_overflow():
     need = max(_need(r, c) for c in cams)
     r.reserve(cams[0], need // 3)
     got = {}
-    for i, img in r.stream_views(cams):
+    for i, img in r.stream_views(cams, pipeline=1):  # one view at a time
         got[i] = img.clone()
     assert sorted(got) == list(range(len(cams)))
     for i in range(len(cams)):
@@ -115,3 +115,23 @@ def test_stale_tape_is_refused():
     ga = splat_backward(scene, cam, None, ta, g["bw_dbuf"])
     gb = splat_backward(scene, cam, None, tb, g["bw_dbuf"])
     assert torch.allclose(ga.positions, gb.positions)
+
+
+def test_pipelined_stream_views_match_and_recover():
+    """Two frames in flight (independent workspaces on their own streams):
+    the same images as one-at-a-time checked renders, also after an
+    overflow restart."""
+    scene = _scene()
+    r = Renderer(scene, pack_atlases(scene), scene.environment, gio.lut())
+    cams = synth.bench_cameras(9, 96, 80)
+    ref = []
+    for c in cams:
+        col, _ = r.render(c, check=True)
+        ref.append(col.cpu().clone())
+    need = max(_need(r, c) for c in cams)
+    for cap in (4 * need, need // 3):
+        r.reserve(cams[0], cap)
+        got = {i: img.clone() for i, img in r.stream_views(cams, pipeline=2)}
+        assert sorted(got) == list(range(len(cams)))
+        for i in range(len(cams)):
+            assert torch.equal(got[i], ref[i]), (cap, i)
