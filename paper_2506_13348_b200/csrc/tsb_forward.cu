@@ -311,13 +311,14 @@ __device__ __forceinline__ void tsb_decode_normal_approx(float ea, float eb, con
   float nx = fmaf(2.0f, ea, -1.0f);
   float ny = fmaf(2.0f, eb, -1.0f);
   const float d2 = fmaf(nx, nx, ny * ny);
+  float nz = 0.0f;  // projected onto the unit disk: |n_xy| = 1, n_z = 0
   if (d2 > 1.0f) {
     const float sc = rsqrt_approx(d2);
     nx *= sc;
     ny *= sc;
+  } else {
+    nz = sqrt_approx(1.0f - d2);
   }
-  const float q = fmaf(-nx, nx, fmaf(-ny, ny, 1.0f));
-  const float nz = sqrt_approx(fmaxf(q, 0.0f));
 #pragma unroll
   for (int i = 0; i < 3; ++i)
     nw[i] = fmaf(nz, frame[6 + i], fmaf(ny, frame[3 + i], nx * frame[i]));
