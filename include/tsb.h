@@ -398,7 +398,7 @@ int tsb_prune_rows(int32_t num_splats, const double* opacities, double threshold
                    const tsb_row_buffer* bufs, int32_t num_bufs, int32_t* kept, void* scratch,
                    uint64_t scratch_bytes, void* stream);
 
-/* ---- Environment precompute (K15-K17) ---------------------------------- */
+/* ---- Environment precompute (K15-K16) ---------------------------------- */
 
 /* Scratch bytes of tsb_env_prefilter for a height x width base map. */
 int tsb_env_scratch_size(int32_t height, int32_t width, uint64_t* bytes);

@@ -2,12 +2,12 @@
 //
 //   K15 k_downsample2     2x2 box average of the base radiance map
 //                         (environment.py:130-135), fp64
-//   K16 k_env_quadrature  per output direction, one warp sums over the
+//   K15 k_env_quadrature  per output direction, one warp sums over the
 //                         downsampled grid: GGX-weighted prefilter of a
 //                         specular level (prefilter_specular :145-175) or the
 //                         cosine-weighted diffuse irradiance
 //                         (diffuse_irradiance :178-195), fp64
-//   K17 k_brdf_lut        split-sum (A, B) per (cos, roughness) cell by GGX
+//   K16 k_brdf_lut        split-sum (A, B) per (cos, roughness) cell by GGX
 //                         importance sampling over a Hammersley set
 //                         (BrdfLut.integrate_cell / build :381-425), fp64
 //

@@ -1,4 +1,4 @@
-"""Environment precompute on the GPU (K15-K17, csrc/tsb_env.cu) against the
+"""Environment precompute on the GPU (K15-K16, csrc/tsb_env.cu) against the
 host restatement, which is bit-identical to the reference's numpy
 (tests/test_host.py pins that). Tolerance: relative 1e-5 of each grid's
 max (fp64 sums in another order, rounded to float32); LUT 1e-9 absolute."""
