@@ -26,6 +26,8 @@ mode = "flat" if a.sampler == "flat" else "atlas"
 r = Renderer(scene, pack_atlases(scene) if mode == "atlas" else None, scene.environment,
              BrdfLut.build(), texture_mode=mode, sampler=None if mode == "flat" else a.sampler,
              texel_format=a.texel_format)
+r.render(cams[0], check=True)
+r.reserve(cams[0], int(r.entries_needed() * 1.25) + 4096)  # as bench.py sizes it
 for i in range(a.frames):
     r.render(cams[i], check=(i == 0))
 torch.cuda.synchronize()
