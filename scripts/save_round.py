@@ -40,7 +40,7 @@ for lname, rname, oname in summ:
 M = ("dram__bytes_read.sum,dram__bytes_write.sum,l1tex__throughput.avg.pct_of_peak_sustained_active,"
      "dram__cycles_active.avg.pct_of_peak_sustained_elapsed,"
      "l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed,gpu__time_duration.sum")
-mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 traffic = {}
 for rname, key in (("full", "cfg2/hw/rgba32f"), ("full_cfg5", "cfg5/hw/rgba32f"),
                    ("full_bwd", "cfg4/k_raster_bwd")):
@@ -60,7 +60,7 @@ for rname, key in (("full", "cfg2/hw/rgba32f"), ("full_cfg5", "cfg5/hw/rgba32f")
         traffic[key.replace("/", "_") + "_ncu"] = {
             "kernel": f"{want} ({key})",
             "duration_us": float(r["gpu__time_duration.sum"]) * {
-                "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}[rows[0]["gpu__time_duration.sum"]],
+                "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}[rows[0]["gpu__time_duration.sum"]],
             "l1tex_throughput_pct": float(r["l1tex__throughput.avg.pct_of_peak_sustained_active"]),
             "tex_data_pipe_pct": float(r["l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed"]),
             "dram_throughput_pct": float(r["dram__cycles_active.avg.pct_of_peak_sustained_elapsed"])}
