@@ -319,6 +319,8 @@ def run_train(args, scene, cams, lut, rank, world, dev):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    n_adam = (len(tr._single_launches()) if world == 1
+              else sum(1 for _, _, n, _ in tr._launches if n))
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -423,7 +425,13 @@ def run_train(args, scene, cams, lut, rank, world, dev):
                     "note": "DataParallelTrainer.step with the view's display target copied "
                             "from pinned host memory and the step's loss terms read back "
                             "every step"},
-            "gpu_launches": None,
+            "gpu_launches": args.steps * (25 + n_adam),
+            "gpu_launches_note": "ours per step: the 13 forward kernels (K1-K6 as in the render "
+                                 "line), 4 x k_ssim_pass, k_shade_bwd, k_env_shard_reduce, "
+                                 "k_reg_count, k_reg_grad, k_raster_bwd, k_finish_grads, "
+                                 "k_guard_finite, k_orthonormalize and k_adam (one launch on one "
+                                 "GPU, one per all-reduce bucket with DP); plus one torch copy "
+                                 "of the fp64 geometry gradients into the flat buffer",
         }
         if world == 1 and not args.no_cpu_baseline and not args.no_numpy_reference:
             line["cpu_baseline"] = numpy_train_timing(args, fragments)
