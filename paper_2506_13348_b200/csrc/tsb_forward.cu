@@ -142,7 +142,11 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   for (int i = threadIdx.x; i <= (int)kRadixBins; i += blockDim.x) s_hx[i] = s_hy[i] = 0;
   if (threadIdx.x == 0) { s_kept = 0; s_total = 0ull; }
   __syncthreads();
-  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  // grid-stride over the splats (the grid is capped at a few CTAs per SM, so
+  // the shared-memory histograms are cleared and merged once per CTA, not
+  // once per 256 splats)
+  for (int id0 = blockIdx.x * blockDim.x; id0 < p.P; id0 += gridDim.x * blockDim.x) {
+  const int id = id0 + threadIdx.x;
   uint32_t kkey = kDepthCulled32, kkept = 0, ktiles = 0;  // this splat's binning facts
   if (id < p.P) {
   const int K = (p.sh_degree + 1) * (p.sh_degree + 1);
@@ -247,6 +251,7 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
     if (lane == 0 && nk) atomicAdd(&s_kept, (int)nk);
     if (lane == 0 && nt) atomicAdd(&s_total, (unsigned long long)nt);
   }
+  }  // grid-stride
   __syncthreads();
   for (int i = threadIdx.x; i < kDepthPasses * (int)kRadixBins; i += blockDim.x) {
     const int v = (&s_hd[0][0])[i];
@@ -914,6 +919,25 @@ static int validate_frame(const tsb_scene* scene, const tsb_camera* camera, cons
   return TSB_OK;
 }
 
+// K1's grid: enough CTAs to fill every SM PREP_WAVES times at TSB_PREP_MINB
+// CTAs per SM; larger scenes loop (grid-stride).
+#ifndef TSB_PREP_WAVES
+#define TSB_PREP_WAVES 2
+#endif
+static int prep_grid_cap() {
+  static PerDevice s_cap;
+  int cap = 0;
+  if (s_cap.get(
+          [](int dev) {
+            int sms = 0;
+            cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            return e == cudaSuccess ? sms * TSB_PREP_MINB * TSB_PREP_WAVES : -(int)e;
+          },
+          &cap) != cudaSuccess)
+    return 148 * TSB_PREP_MINB * TSB_PREP_WAVES;
+  return cap;
+}
+
 int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const tsb_atlas* atlas,
                        int32_t mode, int32_t tile, void* ws, uint64_t ws_bytes, int64_t cap,
                        int64_t* entries_needed, void* stream) {
@@ -956,7 +980,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     pp.slot = scene->record_slot;
     pp.bin = bin;
     pp.total = counters;
-    k_preprocess<<<(P + 255) / 256, 256, 0, st>>>(pp);
+    k_preprocess<<<std::min((P + 255) / 256, prep_grid_cap()), 256, 0, st>>>(pp);
     TSB_CHECK_LAUNCH("k_preprocess");
 
     // S1: depth order (4 one-sweep passes a -> b -> a -> b -> a)
