@@ -241,3 +241,35 @@ def test_train_loop_divergence_guard():
     cfg.iterations = 6
     with pytest.raises(RuntimeError, match="diverged"):
         train(scene, cams, bad, cfg, gio.lut())
+
+
+def test_stage_transition_is_bitwise():
+    """Reference acceptance c06 (pkg/tests/test_acceptance.py:317): growing
+    the trained 1x1 charts to the stage-2 resolution (tsb_broadcast_texels)
+    changes no bit of the rendered images — the first stage-2 render equals
+    the last stage-1 render (fp32 verify-mode sampling of a constant chart is
+    exact)."""
+    from paper_2506_13348_b200.training import (DataParallelTrainer, TrainConfig, train)
+    lut = gio.lut()
+    gt = synth.make_plane_scene(nx=3, ny=3, texture_res=1, seed=2, sh_degree=1)
+    cams = synth.camera_ring(2, radius=3.0, width=32, height=32)
+    targets = [linear_to_display(shade_gbuffer(render_forward(gt, c, "perprim"), c,
+                                               gt.environment, lut,
+                                               background=gt.background).color).cpu().numpy()
+               for c in cams]
+    init = gt.copy()
+    init.positions = init.positions + 0.01
+    cfg = TrainConfig(iterations=6, stage_split=6, texture_resolution=4, seed=3,
+                      prune_interval=100)
+    stage1, _ = train(init, cams, targets, cfg, lut)
+    assert stage1.texture_config.resolution == 1
+    tr = DataParallelTrainer(stage1, lut)
+    tr.broadcast_textures(4)
+    stage2 = tr.to_scene()
+    assert stage2.texture_config.resolution == 4
+    for cam in cams:
+        r1 = shade_gbuffer(render_forward(stage1, cam, "perprim"), cam, stage1.environment, lut,
+                           background=stage1.background).color
+        r2 = shade_gbuffer(render_forward(stage2, cam, "perprim"), cam, stage2.environment, lut,
+                           background=stage2.background).color
+        assert torch.equal(r1, r2)
