@@ -79,7 +79,7 @@ def parse():
     ap.add_argument("--batch-views", type=int, default=0,
                     help="one step = a batch of this many orbit views over all ranks")
     ap.add_argument("--no-numpy-reference", action="store_true")
-    ap.add_argument("--pipeline", type=int, default=3,
+    ap.add_argument("--pipeline", type=int, default=6,
                     help="views in flight: independent workspaces on separate streams "
                          "(1 = one view at a time)")
     a = ap.parse_args()
