@@ -88,6 +88,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // ---------------------------------------------------------------------------
 struct ShadeBwdParams {
   tsb_cam_params cam;
+  ViewCoeffs view;
   tsb_env_params env;
   float bg[3];
   const float* gbuf;
@@ -169,10 +170,10 @@ __device__ void eq_grad(const tsb_grid& g, float* ggrid, bool rgba, float dx, fl
   const float dphi = dfc * ((float)g.w / TWO_PI_F);
   const float zc = dz < -1.0f ? -1.0f : (dz > 1.0f ? 1.0f : dz);
   const bool at_pole = fabsf(dz) >= 1.0f;
-  ddir[2] = at_pole ? 0.0f : -dtheta / sqrtf(1.0f - zc * zc);
-  const float r2 = fmaxf(dx * dx + dy * dy, 1e-30f);
-  ddir[0] = -dy / r2 * dphi;
-  ddir[1] = dx / r2 * dphi;
+  ddir[2] = at_pole ? 0.0f : -dtheta * rsqrtf(1.0f - zc * zc);
+  const float ir2 = __fdividef(1.0f, fmaxf(dx * dx + dy * dy, 1e-30f));
+  ddir[0] = -dy * ir2 * dphi;
+  ddir[1] = dx * ir2 * dphi;
 }
 
 __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
@@ -191,18 +192,18 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
   for (int c = 0; c < 13; ++c) dg[c] = 0.f;
   const float a = g[12];
   if (a > TSB_COVER_EPS) {
-    const int px = pix % W, py = pix / W;
     float wo[3];
-    tsb_view_dir(&p.cam, tsb_pixel_x(&p.cam, px), tsb_pixel_y(&p.cam, py), wo);
+    view_dir_pix(p.view, pix, W, wo);
     const tsb_env_params& env = p.env;
-    const float ia = 1.0f / a;
+    const float ia = __fdividef(1.0f, a);
     const float alb[3] = {g[0] * ia, g[1] * ia, g[2] * ia};
     const float metal = g[3] * ia, rough = g[4] * ia;
     const float nb[3] = {g[5], g[6], g[7]};
     const float nn = sqrtf((nb[0] * nb[0] + nb[1] * nb[1]) + nb[2] * nb[2]);
     const bool degen = nn < 1e-12f;
     float n[3];
-    for (int c = 0; c < 3; ++c) n[c] = degen ? wo[c] : nb[c] / nn;
+    const float rn = degen ? 0.0f : __fdividef(1.0f, nn);  // (tolerance-checked shading)
+    for (int c = 0; c < 3; ++c) n[c] = degen ? wo[c] : nb[c] * rn;
     const float cos_raw = (n[0] * wo[0] + n[1] * wo[1]) + n[2] * wo[2];
     const float cos_cl = cos_raw < TSB_COS_MIN ? TSB_COS_MIN : (cos_raw > 1.0f ? 1.0f : cos_raw);
     float wr[3];
@@ -308,17 +309,17 @@ __global__ void __launch_bounds__(256) k_shade_bwd(ShadeBwdParams p) {
       dn[c] = 2.0f * dwn * wo[c] + 2.0f * cos_raw * dwr[c] + dcos * wo[c] + dn_diff[c];
     if (!degen) {
       const float ndn = (n[0] * dn[0] + n[1] * dn[1]) + n[2] * dn[2];
-      for (int c = 0; c < 3; ++c) dg[5 + c] = (dn[c] - n[c] * ndn) / nn;
+      for (int c = 0; c < 3; ++c) dg[5 + c] = (dn[c] - n[c] * ndn) * rn;
     }
     // de-premultiply
     for (int c = 0; c < 3; ++c) {
-      dg[c] = dalb[c] / a;
-      da -= dalb[c] * alb[c] / a;
+      dg[c] = dalb[c] * ia;
+      da -= dalb[c] * alb[c] * ia;
     }
-    dg[3] = dmetal / a;
-    da -= dmetal * metal / a;
-    dg[4] = drough / a;
-    da -= drough * rough / a;
+    dg[3] = dmetal * ia;
+    da -= dmetal * metal * ia;
+    dg[4] = drough * ia;
+    da -= drough * rough * ia;
     dg[12] = da;
   }
 #pragma unroll
@@ -956,6 +957,7 @@ int tsb_shade_backward(const float* gbuf, const tsb_camera* camera, const tsb_en
                        scratch_bytes >= (uint64_t)kEnvShards * nfl * sizeof(float);
   ShadeBwdParams sp;
   sp.cam = to_cam(camera);
+  sp.view = view_coeffs(camera);
   sp.env.levels = env->levels;
   float* sh = static_cast<float*>(scratch);
   for (int l = 0; l < TSB_MAX_LEVELS; ++l) {

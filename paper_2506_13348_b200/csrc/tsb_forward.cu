@@ -714,47 +714,22 @@ struct ShadeParams {
   tsb_cam_params cam;
   tsb_env_params env;
   float bg[3];
-  // view direction of pixel (px, py) before normalisation: px * vx + py * vy + v0
-  // (splats.py:128-140 folded with the pixel centres; fp32, tolerance-checked)
-  float vx[3], vy[3], v0[3];
-  uint64_t row_magic;  // py = (pix * row_magic) >> 40, exact for pix < 2^24, W < 2^16
+  ViewCoeffs view;  // K6 view directions
   const float* gbuf;
   float* color;
   float* diffuse;
   float* specular;
 };
 
-// The per-camera constants of k_shade's view directions and pixel rows.
-static void shade_view_coeffs(const tsb_camera* camera, ShadeParams* sp) {
-  // x = (px + 0.5 - cx) / fx, y = (py + 0.5 - cy) / fy; d = x R0 + y R1 + R2
-  const double* Wv = camera->world_to_view;
-  for (int j = 0; j < 3; ++j) {
-    sp->vx[j] = (float)(Wv[j] / camera->fx);
-    sp->vy[j] = (float)(Wv[4 + j] / camera->fy);
-    sp->v0[j] = (float)(Wv[8 + j] + Wv[j] * (0.5 - camera->cx) / camera->fx +
-                        Wv[4 + j] * (0.5 - camera->cy) / camera->fy);
-  }
-  sp->row_magic = (((uint64_t)1 << 40) + (uint64_t)camera->width - 1) / (uint64_t)camera->width;
-}
-
 __global__ void __launch_bounds__(256) k_shade(ShadeParams p) {
   const int W = p.cam.width, H = p.cam.height;
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= W * H) return;
-  const int py = (int)(((uint64_t)pix * p.row_magic) >> 40), px = pix - py * W;
   float g[13];
 #pragma unroll
   for (int c = 0; c < 13; ++c) g[c] = __ldg(p.gbuf + (size_t)c * W * H + pix);
   float wo[3];
-  {
-    const float fx = (float)px, fy = (float)py;
-    float d[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) d[j] = fmaf(fy, p.vy[j], fmaf(fx, p.vx[j], p.v0[j]));
-    const float r = -rsqrtf((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) wo[j] = d[j] * r;
-  }
+  view_dir_pix(p.view, pix, W, wo);
   float col[3], dif[3], spe[3];
   tsb_shade_pixel(g, wo, &p.env, p.bg, col, dif, spe);
 #pragma unroll
@@ -1200,7 +1175,7 @@ int tsb_shade_forward(const float* gbuf, const tsb_camera* camera, const tsb_env
   sp.env.lut = env->lut;
   sp.env.lut_res = env->lut_res;
   for (int c = 0; c < 3; ++c) sp.bg[c] = background ? background[c] : 0.f;
-  shade_view_coeffs(camera, &sp);
+  sp.view = view_coeffs(camera);
   sp.gbuf = gbuf; sp.color = color; sp.diffuse = diffuse; sp.specular = specular;
   const int n = camera->width * camera->height;
   k_shade<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(sp);
@@ -1497,7 +1472,7 @@ int tsb_frame_graph_launch(tsb_frame_graph_t g, const tsb_camera* camera, float*
   }
   if (g->n_shade) {
     g->shade.cam = cam;
-    shade_view_coeffs(camera, &g->shade);
+    g->shade.view = view_coeffs(camera);
     if (color) g->shade.color = color;
     void* args[] = {&g->shade};
     cudaKernelNodeParams kp = g->kp_shade;

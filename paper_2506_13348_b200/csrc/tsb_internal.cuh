@@ -359,6 +359,40 @@ struct PerDevice {
   }
 };
 
+// Per-camera constants of the shading kernels' view directions (K6, K7):
+// the unnormalised direction of pixel (px, py) is px * vx + py * vy + v0
+// (splats.py:128-140 folded with the pixel centres (px + 0.5 - cx) / fx;
+// fp32, tolerance-checked), and the pixel row is an exact multiply-shift.
+struct ViewCoeffs {
+  float vx[3], vy[3], v0[3];
+  uint64_t row_magic;  // py = (pix * row_magic) >> 40, exact for pix < 2^24, W < 2^16
+};
+
+inline ViewCoeffs view_coeffs(const tsb_camera* camera) {
+  ViewCoeffs v;
+  const double* Wv = camera->world_to_view;
+  for (int j = 0; j < 3; ++j) {
+    v.vx[j] = (float)(Wv[j] / camera->fx);
+    v.vy[j] = (float)(Wv[4 + j] / camera->fy);
+    v.v0[j] = (float)(Wv[8 + j] + Wv[j] * (0.5 - camera->cx) / camera->fx +
+                      Wv[4 + j] * (0.5 - camera->cy) / camera->fy);
+  }
+  v.row_magic = (((uint64_t)1 << 40) + (uint64_t)camera->width - 1) / (uint64_t)camera->width;
+  return v;
+}
+
+// -omega_o (the unit direction toward the camera) of pixel index pix.
+__device__ __forceinline__ void view_dir_pix(const ViewCoeffs& v, int pix, int W, float* wo) {
+  const int py = (int)(((uint64_t)pix * v.row_magic) >> 40), px = pix - py * W;
+  const float fx = (float)px, fy = (float)py;
+  float d[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) d[j] = fmaf(fy, v.vy[j], fmaf(fx, v.vx[j], v.v0[j]));
+  const float r = -rsqrtf((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) wo[j] = d[j] * r;
+}
+
 void set_error(const std::string& msg);
 int cuda_fail(const char* what, cudaError_t err);
 
