@@ -293,14 +293,12 @@ __global__ void __launch_bounds__(kOsThreads) k_dup_tx(DupArgs a) {
   uint32_t cnt = 0, box = 0;
   int32_t sl = 0;
   if (r < K) {
-    const int id = a.sorted_ids[r];
-    cnt = (uint32_t)a.tile_count[id];
-    if (cnt) {
-      sl = a.slot ? a.slot[id] : id;
-      const uint32_t bx = a.geom[sl].bx, by = a.geom[sl].by;
-      const int tx0 = (int)(bx & 0xFFFF) / a.tile, tx1 = ((int)(bx >> 16) - 1) / a.tile;
-      const int ty0 = (int)(by & 0xFFFF) / a.tile;
-      box = (uint32_t)tx0 | ((uint32_t)ty0 << 8) | ((uint32_t)(tx1 - tx0 + 1) << 16);
+    const uint2 br = a.bin_rec[a.sorted_ids[r]];
+    if (br.y != kBinNoTiles) {
+      sl = (int32_t)br.x;
+      const uint32_t ntx = ((br.y >> 16) & 255u) + 1u, nty = (br.y >> 24) + 1u;
+      cnt = ntx * nty;
+      box = (br.y & 0xFFFFu) | (ntx << 16);
     }
   }
   // the CTA's splats with entries, compacted (draw order kept): entry starts

@@ -56,11 +56,14 @@ struct OnesweepArgs {
   int32_t* ticket;
 };
 
+// k_preprocess's per-splat binning record (by id): .x = record slot, .y =
+// tile box tx0 | ty0 << 8 | (ntx - 1) << 16 | (nty - 1) << 24, or
+// kBinNoTiles (no entries; unambiguous: tx0 + ntx <= 256).
+constexpr uint32_t kBinNoTiles = 0xFFFFFFFFu;
+
 struct DupArgs {
   const int32_t* sorted_ids;
-  const int32_t* tile_count;
-  const int32_t* slot;
-  const GeomRec* geom;
+  const uint2* bin_rec;
   const int32_t* kept;
   const int64_t* total;
   int64_t cap;

@@ -82,7 +82,7 @@ bool ws_layout(int32_t P, int32_t W, int32_t H, int32_t tile, int64_t cap, WsLay
   L->dk32_out = take(Pn * 4);
   L->ids_in = take(Pn * 4);
   L->ids_out = take(Pn * 4);    // the draw order
-  L->tile_count = take(Pn * 4);
+  L->tile_count = take(Pn * 8);  // BinRec (uint2) by id: record slot, tile box
   L->rank = take(Pn * 4);
   L->long_runs = take((Pn / (kShortRun + 2) + 1) * 8);
   L->ekeys_in = take(C * 4);
@@ -122,7 +122,7 @@ struct PrepParams {
   uint32_t* dkey32;
   uint32_t near_hi;      // high word of bits(near)
   int32_t* ids;
-  int32_t* tile_count;
+  uint2* bin_rec;         // by id: (record slot, tile box) for k_dup_tx
   const int32_t* slot;  // record storage permutation (tsb_scene.record_slot) or null
   BinCounters* bin;     // digit histograms, kept count
   int64_t* total;       // entries of the frame (counters[0])
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
                            (uint32_t)r.y0 | ((uint32_t)r.y1 << 16));
   p.ids[id] = id;
   if (!r.keep) {  // culled: no M / frame / SH work, no entries, sorts last
-    p.tile_count[id] = 0;
+    p.bin_rec[id] = make_uint2(0u, kBinNoTiles);
     p.dkeys[id] = ~0ull;
     p.dkey32[id] = kDepthCulled32;
   } else {
@@ -186,18 +186,21 @@ __global__ void __launch_bounds__(256, TSB_PREP_MINB) k_preprocess(PrepParams p)
   // (rasterize.py:246-258) — tiles outside it cannot hold a live pixel.
   const bool binned = tb[1] > tb[0] && tb[3] > tb[2];
   int32_t ntiles = 0;
+  uint32_t tbox = kBinNoTiles;
   if (binned) {
     const int tx0 = tb[0] / p.tile, tx1 = (tb[1] - 1) / p.tile;
     const int ty0 = tb[2] / p.tile, ty1 = (tb[3] - 1) / p.tile;
     const int nx = tx1 - tx0 + 1, ny = ty1 - ty0 + 1;
     ntiles = nx * ny;
+    tbox = (uint32_t)tx0 | ((uint32_t)ty0 << 8) | ((uint32_t)(nx - 1) << 16) |
+           ((uint32_t)(ny - 1) << 24);
     // entries per tile column / row as difference arrays (k_dup_tx, tile-y pass)
     atomicAdd(&s_hx[tx0], ny);
     atomicAdd(&s_hx[tx1 + 1], -ny);
     atomicAdd(&s_hy[ty0], nx);
     atomicAdd(&s_hy[ty1 + 1], -nx);
   }
-  p.tile_count[id] = ntiles;
+  p.bin_rec[id] = make_uint2(binned ? (uint32_t)(p.slot ? p.slot[id] : id) : 0u, tbox);
   // 32-bit depth key: the high word of bits(z) minus that of bits(near) is
   // monotone in z for z > near (positive doubles order like their bit
   // patterns; 2^-20 relative resolution, no clamping); k_fix_runs re-orders
@@ -953,7 +956,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
   uint32_t* k32b = ws_ptr<uint32_t>(ws, L.dk32_in);
   uint32_t* idsa = ws_ptr<uint32_t>(ws, L.ids_out);   // the draw order ends here
   uint32_t* idsb = ws_ptr<uint32_t>(ws, L.ids_in);
-  int32_t* tcount = ws_ptr<int32_t>(ws, L.tile_count);
+  uint2* binrec = ws_ptr<uint2>(ws, L.tile_count);
   int32_t* rank = ws_ptr<int32_t>(ws, L.rank);
   int32_t* ranges = ws_ptr<int32_t>(ws, L.ranges);
   int64_t* counters = ws_ptr<int64_t>(ws, L.counters);
@@ -976,7 +979,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     pp.ids = reinterpret_cast<int32_t*>(idsa);
     pp.dkey32 = k32a;
     pp.near_hi = (uint32_t)(tsb_f64_bits(camera->near_z) >> 32);
-    pp.tile_count = tcount;
+    pp.bin_rec = binrec;
     pp.slot = scene->record_slot;
     pp.bin = bin;
     pp.total = counters;
@@ -1017,7 +1020,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
 
     // S2: tile lists (duplication fused with the tile-x pass, then tile-y)
     DupArgs da;
-    da.sorted_ids = fa.ids; da.tile_count = tcount; da.slot = scene->record_slot; da.geom = geom;
+    da.sorted_ids = fa.ids; da.bin_rec = binrec;
     da.kept = &bin->kept; da.total = counters; da.cap = cap; da.tile = tile;
     da.hist_tx = bin->hist_tx;
     da.kout = ws_ptr<uint32_t>(ws, L.ekeys_in); da.vout = ws_ptr<uint32_t>(ws, L.evals_in);
