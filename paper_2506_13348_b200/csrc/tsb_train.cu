@@ -710,7 +710,7 @@ __global__ void k_prune_gather(int32_t P, const double* __restrict__ op, double 
   const int64_t rb = buf.row_bytes;
   const unsigned char* src = static_cast<const unsigned char*>(buf.src) + (int64_t)i * rb;
   unsigned char* dst = static_cast<unsigned char*>(buf.dst) + dst_row * rb;
-  if ((rb & 7) == 0) {
+  if (((rb | (int64_t)(uintptr_t)buf.src | (int64_t)(uintptr_t)buf.dst) & 7) == 0) {
     for (int64_t q = 0; q < rb / 8; ++q)
       reinterpret_cast<uint64_t*>(dst)[q] = reinterpret_cast<const uint64_t*>(src)[q];
   } else {
