@@ -18,6 +18,14 @@ from .render import Renderer, render
 from .scene import MaterialTextureSet, Scene, TextureConfig
 from .shading import ShadeResult, shade_gbuffer
 from .splats import ALPHA_CUTOFF, DENOM_EPS, SUPPORT_SIGMA, Camera
+# the rest of texsplat's hot-path surface under the same top-level names
+# (texsplat/__init__.py:10-36): adjoints, the training step and loop, formats
+from .backward import SceneGrads, shade_backward, splat_backward
+from .environment import (diffuse_irradiance, equirect_dirs, equirect_solid_angles,
+                          prefilter_specular)
+from .formats import (MissingReferenceError, SchemaError, VersionError, load_atlases,
+                      load_manifest, load_scene, save_atlases, save_manifest, save_scene)
+from .training import (LossWeights, TrainConfig, compute_step, linear_to_display, train)
 
 __version__ = "0.1.0"
 
@@ -28,5 +36,9 @@ __all__ = [
     "GBuffer", "PreparedScene", "Tape", "frame_structure", "prepare", "render_depth_map",
     "render_forward", "render_normal_map", "Renderer", "render", "MaterialTextureSet", "Scene",
     "TextureConfig", "ShadeResult", "shade_gbuffer", "ALPHA_CUTOFF", "DENOM_EPS",
-    "SUPPORT_SIGMA", "Camera", "__version__",
+    "SUPPORT_SIGMA", "Camera", "SceneGrads", "shade_backward", "splat_backward",
+    "diffuse_irradiance", "equirect_dirs", "equirect_solid_angles", "prefilter_specular",
+    "MissingReferenceError", "SchemaError", "VersionError", "load_atlases", "load_manifest",
+    "load_scene", "save_atlases", "save_manifest", "save_scene", "LossWeights", "TrainConfig",
+    "compute_step", "linear_to_display", "train", "__version__",
 ]
