@@ -169,6 +169,66 @@ def cmd_pack_atlas(args) -> int:
     return 0
 
 
+def read_png(path) -> np.ndarray:
+    """PNG as float64 in [0, 1], (H, W) or (H, W, 3) (imgio.py:24-33)."""
+    from PIL import Image
+    with Image.open(path) as im:
+        if im.mode not in ("L", "RGB"):
+            im = im.convert("RGB")
+        return np.asarray(im, dtype=np.float64) / 255.0
+
+
+def _default_init_scene(seed: int):
+    """Neutral-material patch when fit gets no initial scene (cli.py:99-108)."""
+    from . import synth
+    scene = synth.make_plane_scene(nx=6, ny=6, texture_res=1, seed=seed, sh_degree=1,
+                                   textured=False, env_levels=4)
+    scene.texels[...] = np.array([0.5, 0.5, 0.5, 0.5, 0.05, 0.5, 0.5], np.float32)
+    return scene
+
+
+def _train_config(args):
+    """TrainConfig + JSON overrides + --texture-res / --seed (cli.py:111-124)."""
+    from .training import TrainConfig
+    config = TrainConfig()
+    if args.config:
+        for key, value in json.loads(Path(args.config).read_text()).items():
+            if not hasattr(config, key):
+                raise SystemExit(f"unknown config key: {key}")
+            setattr(config, key, value)
+    if args.texture_res is not None:
+        config.texture_resolution = args.texture_res
+    if args.seed is not None:
+        config.seed = args.seed
+    return config
+
+
+def cmd_fit(args) -> int:
+    """Fit a scene to a manifest's images on the GPU (cli.py:127-156): the
+    two-stage train() loop, checkpoint, CSV log, final PSNR / SSIM."""
+    from . import formats
+    from .environment import BrdfLut
+    from .training import evaluate, train
+    if not args.manifest:
+        raise SystemExit("fit requires --manifest")
+    cameras, image_paths = formats.load_manifest(args.manifest)
+    targets = [read_png(p) for p in image_paths]
+    config = _train_config(args)
+    init = formats.load_scene(args.scene) if args.scene else _default_init_scene(config.seed)
+    out_dir = Path(args.out or "fit_out")
+    out_dir.mkdir(parents=True, exist_ok=True)
+    lut = BrdfLut.build(device="cuda")
+    fitted, history = train(init, cameras, targets, config, lut,
+                            log_path=out_dir / "train_log.csv")
+    formats.save_scene(fitted, out_dir / "scene")
+    final = evaluate(fitted, cameras, targets, lut)
+    _emit({"command": "fit", "iterations": config.iterations, "splats": fitted.num_splats,
+           "loss": history[-1]["loss"] if history else None, "psnr": final["psnr"],
+           "ssim": final["ssim"], "checkpoint": str(out_dir / "scene"),
+           "log": str(out_dir / "train_log.csv")})
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="texsplat-b200",
                                      description="Textured 2D Gaussian splats on B200.")
@@ -185,7 +245,7 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--threads", type=int, default=None, help="accepted; the GPU is the pool")
         p.add_argument("--config", help="JSON config overrides")
 
-    for name, fn in (("render", cmd_render), ("bench-atlas", cmd_bench_atlas),
+    for name, fn in (("render", cmd_render), ("fit", cmd_fit), ("bench-atlas", cmd_bench_atlas),
                      ("pack-atlas", cmd_pack_atlas)):
         p = sub.add_parser(name)
         common(p)

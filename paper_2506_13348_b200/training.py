@@ -612,6 +612,58 @@ class DataParallelTrainer:
                      TextureConfig(self.T), environment=env, background=self.background.copy())
 
 
+def _ssim_torch(a: torch.Tensor, b: torch.Tensor) -> float:
+    """Mean SSIM of two (H, W, C) display images (losses.py:61-99: 11-tap
+    sigma-1.5 separable Gaussian, zero padding), float64 on the device — an
+    evaluation metric for `fit`'s summary, not part of the training step."""
+    import torch.nn.functional as F
+    x = torch.arange(-5, 6, dtype=torch.float64, device=a.device)
+    w = torch.exp(-0.5 * (x / 1.5) ** 2)
+    w = w / w.sum()
+    C = a.shape[-1]
+
+    def blur(img):  # (H, W, C) -> (H, W, C)
+        t = img.permute(2, 0, 1).unsqueeze(0)
+        t = F.conv2d(t, w.view(1, 1, 11, 1).expand(C, 1, 11, 1).contiguous(), padding=(5, 0),
+                     groups=C)
+        t = F.conv2d(t, w.view(1, 1, 1, 11).expand(C, 1, 1, 11).contiguous(), padding=(0, 5),
+                     groups=C)
+        return t[0].permute(1, 2, 0)
+
+    mu_a, mu_b = blur(a), blur(b)
+    saa = blur(a * a) - mu_a * mu_a
+    sbb = blur(b * b) - mu_b * mu_b
+    sab = blur(a * b) - mu_a * mu_b
+    c1, c2 = 0.01 ** 2, 0.03 ** 2
+    m = ((2.0 * mu_a * mu_b + c1) * (2.0 * sab + c2)) / (
+        (mu_a * mu_a + mu_b * mu_b + c1) * (saa + sbb + c2))
+    return float(m.mean())
+
+
+def evaluate(scene, cameras, targets_display, lut=None, *, device=None) -> dict:
+    """Mean PSNR / SSIM of a scene against display-space targets
+    (training.py:325-339): each view rendered and shaded on the GPU
+    (per-primitive sampling), display transform, both images clipped to
+    [0, 1]."""
+    from .environment import BrdfLut
+    from .rasterize import render_forward as _rf
+    from .shading import shade_gbuffer as _sg
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    lut = lut if lut is not None else BrdfLut.build(device=dev)
+    ps, ss = [], []
+    for cam, tgt in zip(cameras, targets_display):
+        color = _sg(_rf(scene, cam, "perprim"), cam, scene.environment, lut,
+                    background=scene.background).color
+        disp = linear_to_display(color.to(torch.float64)).clamp(0.0, 1.0)
+        t = _target_tensor(tgt, dev).to(torch.float64)
+        if t.dim() == 2:
+            t = t.unsqueeze(-1).expand(-1, -1, 3)
+        t = t.clamp(0.0, 1.0)
+        ps.append(_psnr_from_mse(float(((disp - t) ** 2).mean())))
+        ss.append(_ssim_torch(disp, t))
+    return {"psnr": float(np.mean(ps)), "ssim": float(np.mean(ss))}
+
+
 def _dist_on() -> bool:
     import torch.distributed as dist
     return dist.is_available() and dist.is_initialized()

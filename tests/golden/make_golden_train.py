@@ -27,7 +27,8 @@ from texsplat.synth import camera_ring, make_plane_scene, render_targets  # noqa
 from texsplat.training import TrainConfig, _texel_tensor, train  # noqa: E402
 
 
-def main():
+def build_inputs():
+    """(lut, init scene, cameras, display targets) of the train-loop fixture."""
     lut = BrdfLut(np.load(HERE / "lut.npz")["table"])
     gt = make_plane_scene(nx=4, ny=3, texture_res=1, seed=2, sh_degree=1)
     cams = camera_ring(3, radius=3.0, width=40, height=40)
@@ -45,6 +46,11 @@ def main():
                  textures=list(init.textures) + list(init.textures[:n_extra]),
                  texture_config=init.texture_config, environment=init.environment,
                  background=init.background)
+    return lut, init, cams, targets
+
+
+def main():
+    lut, init, cams, targets = build_inputs()
     config = TrainConfig(iterations=24, stage_split=12, texture_resolution=4, prune_interval=5,
                          prune_opacity=0.005, seed=4)
     fitted, hist = train(init, cams, targets, config, lut)

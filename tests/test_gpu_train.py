@@ -273,3 +273,45 @@ def test_stage_transition_is_bitwise():
         r2 = shade_gbuffer(render_forward(stage2, cam, "perprim"), cam, stage2.environment, lut,
                            background=stage2.background).color
         assert torch.equal(r1, r2)
+
+
+def test_evaluate_matches_reference():
+    """evaluate() (the GPU render + display transform + clipped PSNR / SSIM of
+    training.py:325-339) vs the reference's on the train-loop fixture's
+    initial scene (tests/golden/make_golden_eval.py)."""
+    from paper_2506_13348_b200.training import evaluate
+    _, scene, cams, targets, _ = _train_golden()
+    ev = gio.load("evaluate")
+    r = evaluate(scene, cams, targets, gio.lut())
+    # fp32 render vs fp64 at ~50 dB: the PSNR moves by thousandths of a dB
+    assert abs(r["psnr"] - float(ev["psnr"])) <= 0.05, (r, float(ev["psnr"]))
+    assert abs(r["ssim"] - float(ev["ssim"])) <= 1e-5, (r, float(ev["ssim"]))
+
+
+def test_fit_cli_end_to_end(tmp_path, capsys):
+    """`cli fit` (cli.py:127-156): manifest + 8-bit PNG targets -> GPU train()
+    -> checkpoint, CSV log and a JSON summary; the checkpoint reloads."""
+    import json
+
+    from paper_2506_13348_b200 import cli, formats
+    _, scene, cams, targets, _ = _train_golden()
+    names = []
+    for i, t in enumerate(targets):
+        name = f"view_{i}.png"
+        cli.write_png(tmp_path / name, np.round(np.clip(t, 0.0, 1.0) * 255.0).astype(np.uint8))
+        names.append(name)
+    formats.save_manifest(tmp_path / "manifest.json", cams, names)
+    formats.save_scene(scene, tmp_path / "init")
+    (tmp_path / "cfg.json").write_text(json.dumps({"iterations": 6, "stage_split": 3,
+                                                    "prune_interval": 100}))
+    rc = cli.main(["fit", "--manifest", str(tmp_path / "manifest.json"), "--scene",
+                   str(tmp_path / "init"), "--out", str(tmp_path / "out"), "--config",
+                   str(tmp_path / "cfg.json"), "--texture-res", "2"])
+    assert rc == 0
+    summary = json.loads(capsys.readouterr().out)
+    assert summary["command"] == "fit" and summary["iterations"] == 6
+    assert np.isfinite(summary["psnr"]) and 0.0 < summary["ssim"] <= 1.0
+    log = (tmp_path / "out" / "train_log.csv").read_text().splitlines()
+    assert len(log) == 1 + 6
+    fitted = formats.load_scene(tmp_path / "out" / "scene")
+    assert fitted.texture_config.resolution == 2 and fitted.num_splats == summary["splats"]
