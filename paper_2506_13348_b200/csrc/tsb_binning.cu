@@ -503,8 +503,8 @@ __global__ void __launch_bounds__(128) k_sort_long_runs(LongRunArgs a) {
   }
 }
 
-template __global__ void k_onesweep<8>(OnesweepArgs a);
-template __global__ void k_onesweep<16>(OnesweepArgs a);
+template __global__ void k_onesweep<kOsItems>(OnesweepArgs a);
+static_assert(kOsItemsDepth == kOsItems, "one instantiation serves both pass kinds");
 
 // K4: tile ranges from the tile-sorted entry keys.
 __global__ void k_ranges(int64_t cap, const uint32_t* __restrict__ keys,

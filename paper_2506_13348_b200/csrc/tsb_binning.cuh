@@ -67,7 +67,6 @@ struct DupArgs {
   const int32_t* kept;
   const int64_t* total;
   int64_t cap;
-  int32_t tile;
   const int32_t* hist_tx;
   uint32_t* kout;
   uint32_t* vout;

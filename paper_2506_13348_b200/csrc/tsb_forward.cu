@@ -1021,7 +1021,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     // S2: tile lists (duplication fused with the tile-x pass, then tile-y)
     DupArgs da;
     da.sorted_ids = fa.ids; da.bin_rec = binrec;
-    da.kept = &bin->kept; da.total = counters; da.cap = cap; da.tile = tile;
+    da.kept = &bin->kept; da.total = counters; da.cap = cap;
     da.hist_tx = bin->hist_tx;
     da.kout = ws_ptr<uint32_t>(ws, L.ekeys_in); da.vout = ws_ptr<uint32_t>(ws, L.evals_in);
     da.status = st_words;
