@@ -664,8 +664,16 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
         // ---- per-splat terms: lane c < 22 sums column c over the live rows
         if (lane < 22) {
           const int nl = __popc(lm);
-          float tot = 0.f;
-          for (int i = 0; i < nl; ++i) tot += ws.red[28 * i + lane];
+          float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;  // four independent chains
+          int i = 0;
+          for (; i + 4 <= nl; i += 4) {
+            t0 += ws.red[28 * i + lane];
+            t1 += ws.red[28 * (i + 1) + lane];
+            t2 += ws.red[28 * (i + 2) + lane];
+            t3 += ws.red[28 * (i + 3) + lane];
+          }
+          for (; i < nl; ++i) t0 += ws.red[28 * i + lane];
+          const float tot = (t0 + t1) + (t2 + t3);
           count_red(p.red_count, tot != 0.0f);
           if (tot != 0.0f) {
             if constexpr (DET)
@@ -696,8 +704,18 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterBwdParams p) {
             leaders &= leaders - 1;
             const uint32_t grp = __shfl_sync(0xffffffffu, peers, l);
             if (lane < 28) {
-              float tsum = 0.f;
-              for (uint32_t m = grp; m; m &= m - 1) tsum += ws.red[36 * (__ffs(m) - 1) + lane];
+              float s0 = 0.f, s1 = 0.f;  // two independent chains over the members
+              uint32_t m = grp;
+              for (; __popc(m) >= 2;) {
+                const int a = __ffs(m) - 1;
+                m &= m - 1;
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                s0 += ws.red[36 * a + lane];
+                s1 += ws.red[36 * b + lane];
+              }
+              if (m) s0 += ws.red[36 * (__ffs(m) - 1) + lane];
+              const float tsum = s0 + s1;
               const int* lr = reinterpret_cast<const int*>(ws.red + 36 * l + 28);
               const int off = lr[0] + ((t_corner & 1) ? lr[1] : 0) + ((t_corner & 2) ? lr[2] : 0) + t_slot;
               count_red(p.red_count, tsum != 0.0f);
