@@ -315,3 +315,32 @@ def test_fit_cli_end_to_end(tmp_path, capsys):
     assert len(log) == 1 + 6
     fitted = formats.load_scene(tmp_path / "out" / "scene")
     assert fitted.texture_config.resolution == 2 and fitted.num_splats == summary["splats"]
+
+
+def test_train_loop_at_scale():
+    """train() on a 20k-splat shell (1x1 charts growing to 8x8 at the stage
+    split, three 256x256 views, pruning on): every logged loss finite, the
+    fit improves, the broadcast and the prune run at scale."""
+    from paper_2506_13348_b200.scene import TextureConfig
+    from paper_2506_13348_b200.training import TrainConfig, train
+    lut = gio.lut()
+    truth = synth.make_shell_scene(20000, 8, seed=5, with_environment=True)
+    cams = synth.bench_cameras(3, 256, 256)
+    targets = [linear_to_display(shade_gbuffer(render_forward(truth, c, "perprim"), c,
+                                               truth.environment, lut,
+                                               background=truth.background).color).cpu().numpy()
+               for c in cams]
+    init = truth.copy()
+    init.positions = init.positions + 0.002
+    init.texels = np.ascontiguousarray(truth.texels.mean(axis=(1, 2), keepdims=True))
+    init.texture_config = TextureConfig(1, truth.texture_config.support)
+    init.opacities[::50] = 0.001  # a few to prune
+    cfg = TrainConfig(iterations=30, stage_split=15, texture_resolution=8, prune_interval=10,
+                      prune_opacity=0.005, seed=1)
+    fitted, hist = train(init, cams, targets, cfg, lut)
+    loss = np.array([h["loss"] for h in hist])
+    assert np.isfinite(loss).all(), loss
+    assert [h["stage"] for h in hist] == [1] * 15 + [2] * 15
+    assert loss[14] < loss[0]
+    assert fitted.texture_config.resolution == 8 and fitted.texels.shape[1:3] == (8, 8)
+    assert fitted.num_splats < init.num_splats  # the near-transparent splats were pruned
