@@ -332,6 +332,12 @@ __device__ __forceinline__ void tsb_decode_normal_approx(float ea, float eb, con
     nw[i] = fmaf(nz, frame[6 + i], fmaf(ny, frame[3 + i], nx * frame[i]));
 }
 
+#ifndef TSB_PAIR_ILP_VERIFY
+#define TSB_PAIR_ILP_VERIFY 1
+#endif
+#ifndef TSB_PAIR_ILP_FLAT
+#define TSB_PAIR_ILP_FLAT 2
+#endif
 #ifndef TSB_PAIR_ILP
 #define TSB_PAIR_ILP 2
 #endif
@@ -613,24 +619,28 @@ k_raster_fwd(RasterParams p) {
         }
       }
 #endif
-      // ---- texture + blend, in order, TSB_PAIR_ILP live pairs per lane per iteration
+      // ---- texture + blend, in order, ILP live pairs per lane per iteration
+      // (verify mode consumes its 8 corner loads inside pair_issue, so a
+      // second pair in flight only costs registers there)
+      constexpr int ILP = MODE == TSB_MODE_VERIFY ? TSB_PAIR_ILP_VERIFY
+                          : MODE == TSB_MODE_FLAT ? TSB_PAIR_ILP_FLAT : TSB_PAIR_ILP;
       while (__any_sync(0xffffffffu, live != 0)) {
 #ifdef TSB_STATS
         if (lane == 0) atomicAdd(&g_tsb_stats[5], 1ull);
 #endif
         if (live) {
-          int kk[TSB_PAIR_ILP];
-          bool hv[TSB_PAIR_ILP];
-          PairFetch f[TSB_PAIR_ILP];
+          int kk[ILP];
+          bool hv[ILP];
+          PairFetch f[ILP];
 #pragma unroll
-          for (int j = 0; j < TSB_PAIR_ILP; ++j) {
+          for (int j = 0; j < ILP; ++j) {
             hv[j] = live != 0;
             kk[j] = hv[j] ? __ffs(live) - 1 : 0;
             live &= live - 1;
             if (hv[j]) pair_issue<MODE>(p, ws, kk[j], make_float2(x, y), f[j]);
           }
 #pragma unroll
-          for (int j = 0; j < TSB_PAIR_ILP; ++j) {
+          for (int j = 0; j < ILP; ++j) {
             if (hv[j] && !done) {
               const int k = kk[j];
               float rv[13];
