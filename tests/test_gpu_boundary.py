@@ -135,3 +135,23 @@ def test_pipelined_stream_views_match_and_recover():
         assert sorted(got) == list(range(len(cams)))
         for i in range(len(cams)):
             assert torch.equal(got[i], ref[i]), (cap, i)
+
+
+def test_integration_md_ctypes_stub_renders_like_the_package():
+    """The ctypes binding INTEGRATION.md shows a texsplat maintainer (section
+    2) runs as written against libtsb.so and gives the package's G-buffer."""
+    import re
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = re.search(r"## 2\..*?```python\n(.*?)```", (root / "INTEGRATION.md").read_text(),
+                     re.S).group(1)
+    code = code.replace('C.CDLL("libtsb.so")',
+                        f'C.CDLL("{root / "paper_2506_13348_b200" / "libtsb.so"}")')
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    scene = _scene()
+    atlas = pack_atlases(scene)
+    cam = synth.bench_cameras(1, 96, 80)[0]
+    got = ns["render_forward_gpu"](scene, cam, atlas)
+    ref = render_forward(scene, cam, "atlas", atlas).data
+    assert torch.equal(got.contiguous(), ref.contiguous())
