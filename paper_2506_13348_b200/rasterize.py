@@ -280,11 +280,17 @@ def render_forward(scene, camera, texture_mode: str = "perprim", atlas_set=None,
                        texel_format=texel_format)
         if not with_tape:
             # no tape outlives the call: the scene's cached workspace serves
-            # every such frame (a tape gets its own, as the reference's tapes
-            # are independent objects)
-            shared = getattr(prep.scene, "_shared_workspace", None)
+            # every such frame on the calling stream (a tape gets its own, as
+            # the reference's tapes are independent objects). One workspace
+            # per stream, so concurrent renders on different streams never
+            # share one (concurrent cameras over one scene).
+            pool = getattr(prep.scene, "_shared_workspaces", None)
+            if pool is None:
+                pool = prep.scene._shared_workspaces = {}
+            key = _lib.stream_handle(None) or 0
+            shared = pool.get(key)
             if shared is None:
-                shared = prep.scene._shared_workspace = prep.workspace
+                shared = pool[key] = prep.workspace
             prep.workspace = shared
     gbuf, tape = render_prepared(prep, camera, tile)
     return (gbuf, tape) if with_tape else gbuf
