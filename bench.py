@@ -425,9 +425,9 @@ def run_train(args, scene, cams, lut, rank, world, dev):
                     "note": "DataParallelTrainer.step with the view's display target copied "
                             "from pinned host memory and the step's loss terms read back "
                             "every step"},
-            "gpu_launches": args.steps * (25 + n_adam),
+            "gpu_launches": args.steps * (24 + n_adam),
             "gpu_launches_note": "ours per step: the 13 forward kernels (K1-K6 as in the render "
-                                 "line), 4 x k_ssim_pass, k_shade_bwd, k_env_shard_reduce, "
+                                 "line), 3 K10 SSIM passes, k_shade_bwd, k_env_shard_reduce, "
                                  "k_reg_count, k_reg_grad, k_raster_bwd, k_finish_grads, "
                                  "k_guard_finite, k_orthonormalize and k_adam (one launch on one "
                                  "GPU, one per all-reduce bucket with DP); plus one torch copy "

@@ -182,61 +182,55 @@ __global__ void __launch_bounds__(256) k_ssim_pass2(int W, int H, const float* _
   block_sums_atomic(msum, terms + 1);
 }
 
-// ---- K10 pass 3: horizontal blur of the 9 adjoint planes.
-__global__ void __launch_bounds__(256) k_ssim_pass3(int W, int H, const float* __restrict__ part,
-                                                    float* __restrict__ out) {
-  __shared__ float sp[256 + 2 * kR];
-  const int y = blockIdx.y, plane = blockIdx.z;
-  const int x0 = blockIdx.x * 256, x = x0 + threadIdx.x;
+// ---- K10 passes 3+4 fused: the horizontal blur of the three adjoint planes
+// of one channel goes to shared memory (rows with a 5-row halo) and the
+// vertical blur reads it there, so the blurred planes never go through HBM.
+// Same sums in the same order as separate passes (zero padding outside).
+constexpr int kFTY = 32, kFR = kFTY + 2 * kR, kFX = 32, kFC = kFX + 2 * kR;
+__global__ void __launch_bounds__(256) k_ssim_pass34(int W, int H, const float* __restrict__ part,
+                                                     const float* __restrict__ color,
+                                                     const float* __restrict__ target,
+                                                     float l1_scale, float* __restrict__ dcolor) {
+  __shared__ float raw[3][kFR][kFC + 1];
+  __shared__ float hbt[3][kFR][kFX + 1];
+  const int x0 = blockIdx.x * kFX, y0 = blockIdx.y * kFTY, c = blockIdx.z;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const size_t HW = (size_t)W * H;
-  const float* src = part + plane * HW + (size_t)y * W;
-  for (int i = threadIdx.x; i < 256 + 2 * kR; i += 256) {
-    const int xx = x0 - kR + i;
-    sp[i] = (xx >= 0 && xx < W) ? src[xx] : 0.0f;
+  for (int i = threadIdx.x; i < 3 * kFR * kFC; i += blockDim.x) {
+    const int pl = i / (kFR * kFC), r = (i / kFC) % kFR, cx = i % kFC;
+    const int yy = y0 - kR + r, xx = x0 - kR + cx;
+    raw[pl][r][cx] = (yy >= 0 && yy < H && xx >= 0 && xx < W)
+                         ? part[(size_t)(3 * c + pl) * HW + (size_t)yy * W + xx] : 0.0f;
   }
   __syncthreads();
-  if (x >= W) return;
-  float s = 0.f;
+  for (int i = threadIdx.x; i < 3 * kFR * kFX; i += blockDim.x) {
+    const int pl = i / (kFR * kFX), r = (i / kFX) % kFR, cx = i % kFX;
+    float h = 0.f;
 #pragma unroll
-  for (int t = 0; t <= 2 * kR; ++t) s += c_win[t] * sp[threadIdx.x + t];
-  out[plane * HW + (size_t)y * W + x] = s;
-}
-
-// ---- K10 pass 4: vertical blur of the adjoints and the colour gradient:
-// d(pred) = (1-w) sign(a-b)/N + blur(g_mu_a) + 2a blur(g_saa) + b blur(g_sab),
-// dcolor = d(pred) * display'(color).
-__global__ void __launch_bounds__(256) k_ssim_pass4(int W, int H, const float* __restrict__ hb,
-                                                    const float* __restrict__ color,
-                                                    const float* __restrict__ target,
-                                                    float l1_scale, float* __restrict__ dcolor) {
-  __shared__ float tile[3][kTR][kTX + 1];
-  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int t = 0; t <= 2 * kR; ++t) h += c_win[t] * raw[pl][r][cx + t];
+    const int yy = y0 - kR + r;
+    hbt[pl][r][cx] = (yy >= 0 && yy < H) ? h : 0.0f;
+  }
+  __syncthreads();
   const int x = x0 + tx;
-  const size_t HW = (size_t)W * H;
-  {
-    const int c = blockIdx.z;  // one colour channel per CTA layer
-    stage_vtile<3>(tile, hb + (size_t)(3 * c) * HW, HW, W, H, x0, y0);
-    __syncthreads();
-    for (int r = ty; r < kTY; r += 8) {
-      const int y = y0 + r;
-      if (y >= H || x >= W) continue;
-      float v[3] = {0.f, 0.f, 0.f};
+  for (int r = ty; r < kFTY; r += 8) {
+    const int y = y0 + r;
+    if (y >= H || x >= W) continue;
+    float v[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-      for (int t = 0; t <= 2 * kR; ++t) {
-        const float w = c_win[t];
-        v[0] += w * tile[0][r + t][tx];
-        v[1] += w * tile[1][r + t][tx];
-        v[2] += w * tile[2][r + t][tx];
-      }
-      const size_t pix = (size_t)y * W + x;
-      const float cx = color[3 * pix + c];
-      const float a = display_of(cx), b = target[3 * pix + c];
-      const float d = a - b;
-      const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-      const float dpred = l1_scale * sg + v[0] + 2.0f * a * v[1] + b * v[2];
-      dcolor[3 * pix + c] = dpred * display_slope(cx);
+    for (int t = 0; t <= 2 * kR; ++t) {
+      const float w = c_win[t];
+      v[0] += w * hbt[0][r + t][tx];
+      v[1] += w * hbt[1][r + t][tx];
+      v[2] += w * hbt[2][r + t][tx];
     }
+    const size_t pix = (size_t)y * W + x;
+    const float cx = color[3 * pix + c];
+    const float a = display_of(cx), b = target[3 * pix + c];
+    const float d = a - b;
+    const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+    const float dpred = l1_scale * sg + v[0] + 2.0f * a * v[1] + b * v[2];
+    dcolor[3 * pix + c] = dpred * display_slope(cx);
   }
 }
 
@@ -772,7 +766,6 @@ int tsb_loss_image(const float* color, const float* target, int32_t width, int32
   TSB_CUDA(ensure_window());
   float* m5 = static_cast<float*>(scratch);
   float* part = m5 + 15 * HW;
-  float* hb = m5;  // pass 3 output reuses the moment planes
   const double N = 3.0 * (double)HW;
   const dim3 rows((width + 255) / 256, height);
   const dim3 strips((width + 255) / 256, (height + kRowsPerBlock - 1) / kRowsPerBlock);
@@ -782,11 +775,9 @@ int tsb_loss_image(const float* color, const float* target, int32_t width, int32
   k_ssim_pass2<<<vtiles, 256, 0, st>>>(width, height, m5, part,
                                      (float)(-0.5 * dssim_weight / N), terms);
   TSB_CHECK_LAUNCH("k_ssim_pass2");
-  k_ssim_pass3<<<dim3((width + 255) / 256, height, 9), 256, 0, st>>>(width, height, part, hb);
-  TSB_CHECK_LAUNCH("k_ssim_pass3");
-  k_ssim_pass4<<<vtiles, 256, 0, st>>>(width, height, hb, color, target,
-                                     (float)((1.0 - dssim_weight) / N), dcolor);
-  TSB_CHECK_LAUNCH("k_ssim_pass4");
+  k_ssim_pass34<<<dim3((width + kFX - 1) / kFX, (height + kFTY - 1) / kFTY, 3), 256, 0, st>>>(
+      width, height, part, color, target, (float)((1.0 - dssim_weight) / N), dcolor);
+  TSB_CHECK_LAUNCH("k_ssim_pass34");
   return TSB_OK;
 }
 
