@@ -155,6 +155,7 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* wrun, uint32_t d, int la
 // ---------------------------------------------------------------------------
 template <int ITEMS>
 __global__ void __launch_bounds__(kOsThreads) k_onesweep(OnesweepArgs a) {
+  pdl_wait();
   constexpr int TILE = kOsThreads * ITEMS;
   constexpr uint32_t kCulledBin = kRadixBins;  // depth pass 1: culled items' own counter
   __shared__ uint32_t whist[kOsWarps][kRadixBins + 1];
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(kOsThreads) k_onesweep(OnesweepArgs a) {
 // scatters (tile_y << 8 | tile_x, record slot) stably by tile_x.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kOsThreads) k_dup_tx(DupArgs a) {
+  pdl_wait();
   __shared__ uint32_t whist[kOsWarps][kRadixBins + 1];
   __shared__ uint32_t s_goff[kRadixBins];
   __shared__ uint32_t s_base[kOsThreads + 33];
@@ -398,6 +400,7 @@ __global__ void __launch_bounds__(kOsThreads) k_dup_tx(DupArgs a) {
 // order inside a run is id order (stable passes over id-ordered input).
 // ---------------------------------------------------------------------------
 __global__ void k_fix_runs(FixRunsArgs a) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.P) return;
   const uint32_t k = a.k32[i];
@@ -440,6 +443,7 @@ __global__ void k_fix_runs(FixRunsArgs a) {
 // key (the high word is the run's common key), ids ping-ponging through
 // `scratch`. O(run) per pass; then the ranks.
 __global__ void __launch_bounds__(128) k_sort_long_runs(LongRunArgs a) {
+  pdl_wait();
   __shared__ uint32_t run_ctr[4][kRadixBins + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * 4 + w, nw = gridDim.x * 4;
@@ -510,6 +514,7 @@ static_assert(kOsItemsDepth == kOsItems, "one instantiation serves both pass kin
 __global__ void k_ranges(int64_t cap, const uint32_t* __restrict__ keys,
                          const int64_t* __restrict__ counters, int32_t* __restrict__ ranges,
                          int64_t* __restrict__ max_needed) {
+  pdl_wait();
   int64_t total = counters[0];
   if (blockIdx.x == 0 && threadIdx.x == 0)  // running max (tsb_frame_workspace_max_needed_offset)
     atomicMax(reinterpret_cast<unsigned long long*>(max_needed), (unsigned long long)total);

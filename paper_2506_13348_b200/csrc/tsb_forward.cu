@@ -494,6 +494,7 @@ __device__ __forceinline__ void pair_result(const WarpSmem<MODE>& ws, const Pair
 template <int TILE, int MODE>
 __global__ void __launch_bounds__(32 * TSB_RASTER_WARPS, TSB_RASTER_MINB)
 k_raster_fwd(RasterParams p) {
+  pdl_wait();
   constexpr int NBLK = TILE * TILE / 32;  // 8 x 4 pixel blocks per tile
   constexpr int WX = TILE / 8;            // blocks per tile row
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -686,7 +687,10 @@ k_raster_fwd(RasterParams p) {
 constexpr int kSchedThreads = 1024;
 __global__ void __launch_bounds__(kSchedThreads) k_tile_schedule(int32_t nt,
                                                                  const int32_t* __restrict__ ranges,
-                                                                 int32_t* __restrict__ order) {
+                                                                 int32_t* __restrict__ order,
+                                                                 int32_t* __restrict__ work_counter) {
+  pdl_wait();
+  if (threadIdx.x == 0) *work_counter = 0;  // K5's unit counter (K5 waits for this kernel)
   __shared__ int cursor[kSchedThreads];
   __shared__ int wsum[kSchedThreads / 32];
   const int tid = threadIdx.x;
@@ -735,6 +739,7 @@ struct ShadeParams {
 };
 
 __global__ void __launch_bounds__(256) k_shade(ShadeParams p) {
+  pdl_wait();
   const int W = p.cam.width, H = p.cam.height;
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= W * H) return;
@@ -843,8 +848,7 @@ inline cudaError_t launch_raster_mode(int blocks, cudaStream_t st, const RasterP
   // one warp per (tile, 8x4 block) unit at most
   const int units = blocks * (TILE * TILE / 32);
   const int grid = std::min((units + TSB_RASTER_WARPS - 1) / TSB_RASTER_WARPS, resident);
-  k_raster_fwd<TILE, MODE><<<grid, threads, smem, st>>>(rp);
-  return cudaGetLastError();
+  return launch_pdl(k_raster_fwd<TILE, MODE>, grid, threads, smem, st, rp);
 }
 
 template <int TILE>
@@ -1013,19 +1017,19 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
       oa.mode = q == 0 ? kOsFirst : kOsLater;
       oa.kept = &bin->kept;
       oa.ticket = &bin->tickets[q];
-      k_onesweep<kOsItemsDepth><<<L.nb_depth, kOsThreads, 0, st>>>(oa);
+      TSB_CUDA(launch_pdl(k_onesweep<kOsItemsDepth>, L.nb_depth, kOsThreads, 0, st, oa));
       TSB_CHECK_LAUNCH("k_onesweep(depth)");
       st_words += pass_status_words(L.nb_depth);
     }
     FixRunsArgs fa;
     fa.P = P; fa.k32 = k32a; fa.k64 = dk64; fa.ids = reinterpret_cast<int32_t*>(idsa);
     fa.rank = rank; fa.n_long = &bin->n_long; fa.long_runs = ws_ptr<int32_t>(ws, L.long_runs);
-    k_fix_runs<<<(P + 255) / 256, 256, 0, st>>>(fa);
+    TSB_CUDA(launch_pdl(k_fix_runs, (P + 255) / 256, 256, 0, st, fa));
     TSB_CHECK_LAUNCH("k_fix_runs");
     LongRunArgs la;
     la.n_long = &bin->n_long; la.long_runs = fa.long_runs; la.k64 = dk64;
     la.ids = fa.ids; la.scratch = ws_ptr<int32_t>(ws, L.dkeys_out); la.rank = rank;
-    k_sort_long_runs<<<16, 128, 0, st>>>(la);
+    TSB_CUDA(launch_pdl(k_sort_long_runs, 16, 128, 0, st, la));
     TSB_CHECK_LAUNCH("k_sort_long_runs");
 
     // S2: tile lists (duplication fused with the tile-x pass, then tile-y)
@@ -1037,7 +1041,7 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     da.status = st_words;
     da.nb = L.nb_dup;
     da.ticket = &bin->tickets[4];
-    k_dup_tx<<<L.nb_dup, kOsThreads, 0, st>>>(da);
+    TSB_CUDA(launch_pdl(k_dup_tx, L.nb_dup, kOsThreads, 0, st, da));
     TSB_CHECK_LAUNCH("k_dup_tx");
     st_words += pass_status_words(L.nb_dup);
     OnesweepArgs ya;
@@ -1053,12 +1057,12 @@ int tsb_render_binning(const tsb_scene* scene, const tsb_camera* camera, const t
     ya.mode = kOsPlain;
     ya.kept = nullptr;
     ya.ticket = &bin->tickets[5];
-    k_onesweep<kOsItems><<<L.nb_tiley, kOsThreads, 0, st>>>(ya);
+    TSB_CUDA(launch_pdl(k_onesweep<kOsItems>, L.nb_tiley, kOsThreads, 0, st, ya));
     TSB_CHECK_LAUNCH("k_onesweep(tile_y)");
     const int64_t C = std::max<int64_t>(cap, 1);
-    k_ranges<<<(unsigned)std::min<int64_t>((C + 255) / 256, 148 * 16), 256, 0, st>>>(
-        cap, ya.kout, counters, ranges,
-                                                          ws_ptr<int64_t>(ws, L.max_needed));
+    TSB_CUDA(launch_pdl(k_ranges, (unsigned)std::min<int64_t>((C + 255) / 256, 148 * 16), 256,
+                        0, st, (int64_t)cap, (const uint32_t*)ya.kout, (const int64_t*)counters,
+                        ranges, ws_ptr<int64_t>(ws, L.max_needed)));
     TSB_CHECK_LAUNCH("k_ranges");
   }
   if (entries_needed)
@@ -1101,10 +1105,10 @@ int tsb_render_composite(const tsb_scene* scene, const tsb_camera* camera, const
   rp.touched = px->splat_touched;
   rp.num_tiles = L.num_tiles;
   rp.work_counter = reinterpret_cast<int32_t*>(ws_ptr<int64_t>(ws, L.counters) + 1);
-  TSB_CUDA(cudaMemsetAsync(rp.work_counter, 0, 4, st));
   rp.tile_order = nullptr;
-  k_tile_schedule<<<1, kSchedThreads, 0, st>>>(L.num_tiles, rp.ranges,
-                                               ws_ptr<int32_t>(ws, L.torder_out));
+  TSB_CUDA(launch_pdl(k_tile_schedule, 1, kSchedThreads, 0, st, (int32_t)L.num_tiles,
+                      (const int32_t*)rp.ranges, ws_ptr<int32_t>(ws, L.torder_out),
+                      rp.work_counter));
   TSB_CHECK_LAUNCH("k_tile_schedule");
   rp.tile_order = ws_ptr<int32_t>(ws, L.torder_out);
   cudaError_t e;
@@ -1191,7 +1195,7 @@ int tsb_shade_forward(const float* gbuf, const tsb_camera* camera, const tsb_env
   sp.view = view_coeffs(camera);
   sp.gbuf = gbuf; sp.color = color; sp.diffuse = diffuse; sp.specular = specular;
   const int n = camera->width * camera->height;
-  k_shade<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(sp);
+  TSB_CUDA(launch_pdl(k_shade, (n + 255) / 256, 256, 0, (cudaStream_t)stream, sp));
   TSB_CHECK_LAUNCH("k_shade");
   return TSB_OK;
 }

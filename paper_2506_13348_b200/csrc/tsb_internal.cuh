@@ -393,6 +393,42 @@ __device__ __forceinline__ void view_dir_pix(const ViewCoeffs& v, int pix, int W
   for (int j = 0; j < 3; ++j) wo[j] = d[j] * r;
 }
 
+// Programmatic dependent launch (sm_90+): a frame's kernels are launched
+// with programmatic stream serialisation, so each one's CTAs are scheduled
+// while its predecessor drains and wait in pdl_wait() (griddepcontrol.wait:
+// the predecessor has completed and its writes are visible) instead of
+// paying a full launch gap per kernel. Every such kernel calls pdl_wait()
+// before touching its predecessor's output (a no-op without the attribute).
+#ifndef TSB_PDL
+#define TSB_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if TSB_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+#if TSB_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+#else
+  kernel<<<grid, block, smem, st>>>(args...);
+  return cudaGetLastError();
+#endif
+}
+
 void set_error(const std::string& msg);
 int cuda_fail(const char* what, cudaError_t err);
 
